@@ -1,0 +1,31 @@
+#!/usr/bin/env bash
+# ORACLE TEST INFRASTRUCTURE — builds the reference CPU path from its own,
+# unmodified sources where they lie (/root/reference/proj/src), plus our
+# FFTW-API shim (oracle/fftw_shim) and the extern "C" test wrapper
+# (oracle/ref_capi.cpp), into oracle/_ref/libptychodd_ref.so.
+#
+# Flags follow the reference's Release default (proj/CMakeLists.txt:6-8:
+# -O3 -DNDEBUG, C++20, no -march).  io.cpp is left out: PTYA/JSON/PNG I/O is
+# out of scope and would need zlib + nlohmann/json.  Output goes only to
+# oracle/_ref/ (git-ignored; it travels to the GPU box with the snapshot).
+set -euo pipefail
+here="$(cd "$(dirname "$0")" && pwd)"
+ref="${PDD_REFERENCE:-/root/reference}/proj"
+out="$here/_ref"
+if [ ! -d "$ref/src" ]; then
+  echo "build_ref.sh: reference sources not found at $ref (skipping)" >&2
+  exit 0
+fi
+mkdir -p "$out"
+srcs=(field fft scan forward stagm ddplan solver blind simulate metrics)
+objs=()
+for s in "${srcs[@]}"; do
+  o="$out/ref_$s.o"
+  g++ -std=c++20 -O3 -DNDEBUG -fPIC -I"$ref/include" -I"$here/fftw_shim" -c "$ref/src/$s.cpp" -o "$o"
+  objs+=("$o")
+done
+g++ -std=c++20 -O3 -DNDEBUG -fPIC -c "$here/fftw_shim/fftw_shim.cpp" -o "$out/fftw_shim.o"
+g++ -std=c++20 -O3 -DNDEBUG -fPIC -I"$ref/include" -I"$here/fftw_shim" -c "$here/ref_capi.cpp" -o "$out/ref_capi.o"
+g++ -shared -o "$out/libptychodd_ref.so" "${objs[@]}" "$out/fftw_shim.o" "$out/ref_capi.o" -lpthread
+rm -f "$out"/*.o
+echo "built $out/libptychodd_ref.so"

@@ -1,0 +1,294 @@
+// Per-rank device resources shared by the nonblind and blind drivers:
+// measured amplitudes, frame/tile/pair tables, reduction scratch, iteration
+// control, and the setup computations of the reference constructors
+// (frame partitioning, pins, R-factor denominator).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <vector>
+
+#include "device.hpp"
+#include "engine.hpp"
+#include "frame_kernel.cuh"
+#include "kernels.hpp"
+#include "layout.hpp"
+
+namespace pdd {
+
+template <typename T>
+std::vector<cx<T>> to_cx(const double* p, int64_t n) {
+  std::vector<cx<T>> v(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) v[i] = cx<T>{static_cast<T>(p[2 * i]), static_cast<T>(p[2 * i + 1])};
+  return v;
+}
+
+template <typename T>
+void from_cx(const std::vector<cx<T>>& v, double* out) {
+  for (size_t i = 0; i < v.size(); ++i) {
+    out[2 * i] = static_cast<double>(v[i].x);
+    out[2 * i + 1] = static_cast<double>(v[i].y);
+  }
+}
+
+template <typename T>
+std::vector<cx<T>> twiddles(int S) {
+  std::vector<cx<T>> w(static_cast<size_t>(S));
+  for (int k = 0; k < S; ++k) {
+    const double a = -2.0 * M_PI * static_cast<double>(k) / static_cast<double>(S);
+    w[k] = cx<T>{static_cast<T>(std::cos(a)), static_cast<T>(std::sin(a))};
+  }
+  return w;
+}
+
+template <typename T>
+std::vector<cx<T>> download_cx(const void* dev, int64_t n, cudaStream_t st) {
+  std::vector<cx<T>> h(static_cast<size_t>(n));
+  if (n > 0) PDD_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(cx<T>) * n, cudaMemcpyDeviceToHost, st));
+  PDD_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+template <typename T>
+void upload_cx(void* dev, const double* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  auto h = to_cx<T>(src, n);
+  PDD_CUDA(cudaMemcpyAsync(dev, h.data(), sizeof(cx<T>) * n, cudaMemcpyHostToDevice, st));
+  PDD_CUDA(cudaStreamSynchronize(st));
+}
+
+template <typename T>
+struct RankData {
+  Layout L;
+  int S = 0, device = 0;
+  Comm* comm = nullptr;
+  Stream stream;
+  DevMem amp, tw;
+  DevMem fr_off, fr_pitch, fr_r, fr_c, fr_sub;
+  DevMem tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg, psides, pgeom;
+  DevMem sub_fr_beg, sub_tile_beg, local_map;
+  DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
+  DevMem ctl, rec;
+  std::vector<std::vector<uint8_t>> pins;  // per local subdomain
+  double l1 = 0.0;
+  int D = 0;
+  int rec_cap = 0;
+
+  cudaStream_t st() const { return stream.get(); }
+  int64_t SS() const { return static_cast<int64_t>(S) * S; }
+  double* rf_sub() const { return sums.as<double>(); }
+  double* diff_sub() const { return sums.as<double>() + D; }
+  double* norm_sub() const { return sums.as<double>() + 2 * D; }
+  RunCtl* ctlp() const { return ctl.as<RunCtl>(); }
+  int* skipA() const { return &ctl.as<RunCtl>()->skipA; }
+  int* skipB() const { return &ctl.as<RunCtl>()->skipB; }
+
+  void build(const Plan& plan, const DataSpec& data, const double* pin_ones, int dev, Comm* c, int max_iters,
+             const char* who) {
+    device = dev;
+    comm = c;
+    const int rank = c ? c->rank() : 0, world = c ? c->world() : 1;
+    L = Layout::build(plan, rank, world);
+    S = L.S;
+    D = plan.D;
+    if (!frame_supported<T>(S))
+      throw InvalidArgument(std::string(who) + ": frame side " + std::to_string(S) +
+                            " not supported by the CUDA path (powers of two up to " +
+                            (sizeof(T) == 4 ? "128" : "64") + ")");
+    cudaStream_t s = st();
+    tw = upload(twiddles<T>(S), s);
+    fr_off = upload(L.fr_off, s);
+    fr_pitch = upload(L.fr_pitch, s);
+    fr_r = upload(L.fr_r, s);
+    fr_c = upload(L.fr_c, s);
+    fr_sub = upload(L.fr_sub, s);
+    tiles = upload(L.tiles, s);
+    tile_frames = upload(L.tile_frames, s);
+    sub_off = upload(L.sub_img_off, s);
+    sub_h = upload(L.sub_h, s);
+    sub_w = upload(L.sub_w, s);
+    sub_pbeg = upload(L.sub_pbeg, s);
+    psides = upload(L.psides, s);
+    pgeom = upload(L.pgeom, s);
+    sub_fr_beg = upload(L.sub_fr_beg, s);
+    sub_tile_beg = upload(L.sub_tile_beg, s);
+    local_map = upload(L.local_subs, s);
+    rf_part.alloc(sizeof(double) * std::max<int64_t>(L.nfr, 1));
+    re_part.alloc(sizeof(double) * 2 * std::max(L.ntiles(), 1));
+    sums.alloc(sizeof(double) * 3 * D);
+    PDD_CUDA(cudaMemsetAsync(sums.get(), 0, sums.bytes(), s));
+    ctl.alloc(sizeof(RunCtl));
+    PDD_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(RunCtl), s));
+    rec_cap = max_iters + 2;
+    rec.alloc(sizeof(double) * 2 * static_cast<size_t>(rec_cap));
+
+    upload_amplitudes(plan, data);
+    build_pins(plan, pin_ones);
+  }
+
+  // Measured data -> T amplitudes in local frame order, plus the R-factor
+  // denominator sum sqrt(f) (solver.cpp:80-93).
+  void upload_amplitudes(const Plan& plan, const DataSpec& data) {
+    cudaStream_t s = st();
+    const int64_t per = SS();
+    amp.alloc(sizeof(T) * std::max<int64_t>(L.nfr * per, 1));
+    const size_t esz = data.kind == kAmplitudeF32 ? 4 : 8;
+    const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (per * static_cast<int64_t>(esz)));
+    DevMem stage(esz * static_cast<size_t>(std::min(chunk, std::max<int64_t>(L.nfr, 1)) * per));
+    DevMem neg(sizeof(unsigned long long));
+    PDD_CUDA(cudaMemsetAsync(neg.get(), 0, neg.bytes(), s));
+    const cudaMemcpyKind kind = data.device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const char* src = static_cast<const char*>(data.ptr);
+    for (int64_t f0 = 0; f0 < L.nfr; f0 += chunk) {
+      const int64_t f1 = std::min(L.nfr, f0 + chunk);
+      int64_t f = f0;
+      while (f < f1) {  // runs of consecutive global frames
+        int64_t e = f + 1;
+        while (e < f1 && L.fr_global[e] == L.fr_global[e - 1] + 1) ++e;
+        PDD_CUDA(cudaMemcpyAsync(stage.as<char>() + (f - f0) * per * esz, src + L.fr_global[f] * per * esz,
+                                 (e - f) * per * esz, kind, s));
+        f = e;
+      }
+      PDD_CUDA(launch_convert_amp<T>(stage.get(), data.kind, amp.as<T>() + f0 * per, (f1 - f0) * per,
+                                     neg.as<unsigned long long>(), s));
+      PDD_CUDA(cudaStreamSynchronize(s));  // stage reuse
+    }
+    unsigned long long nneg = 0;
+    PDD_CUDA(cudaMemcpy(&nneg, neg.get(), sizeof(nneg), cudaMemcpyDeviceToHost));
+    if (nneg) throw InvalidArgument("FrameStack: negative intensity");
+    // l1 = sum_d sum_j sum_i sqrt(f)
+    DevMem fs(sizeof(double) * std::max<int64_t>(L.nfr, 1));
+    PDD_CUDA(launch_frame_sums<T>(amp.as<T>(), L.nfr, per, fs.as<double>(), s));
+    PDD_CUDA(launch_segsum(fs.as<double>(), 1, 0, sub_fr_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                           rf_sub(), nullptr, s));
+    if (comm) comm->allreduce_sum_f64(rf_sub(), D, s);
+    std::vector<double> per_sub(D);
+    PDD_CUDA(cudaMemcpyAsync(per_sub.data(), rf_sub(), sizeof(double) * D, cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
+    l1 = 0.0;
+    for (double x : per_sub) l1 += x;
+    PDD_CUDA(cudaMemsetAsync(sums.get(), 0, sums.bytes(), s));
+  }
+
+  // Pixels never covered by a window, plus the caller's vacuum mask
+  // (solver.cpp:43-48, 64-69).
+  void build_pins(const Plan& plan, const double* pin_ones) {
+    const auto cov = scan_coverage(plan.g);
+    pins.clear();
+    for (int ld = 0; ld < L.nls(); ++ld) {
+      const Rect& sub = plan.subs[L.local_subs[ld]];
+      std::vector<uint8_t> p(static_cast<size_t>(sub.area()));
+      for (int64_t r = 0; r < sub.h(); ++r)
+        for (int64_t c = 0; c < sub.w(); ++c) {
+          const int64_t gi = (sub.r0 + r) * plan.g.W + sub.c0 + c;
+          p[r * sub.w() + c] = cov[gi] == 0 || (pin_ones && pin_ones[gi] > 0.5);
+        }
+      pins.push_back(std::move(p));
+    }
+  }
+
+  FrameArgs<T> frame_args() const {
+    FrameArgs<T> a;
+    a.nframes = static_cast<int>(L.nfr);
+    a.tw = tw.as<cx<T>>();
+    a.off = fr_off.as<int64_t>();
+    a.pitch = fr_pitch.as<int32_t>();
+    a.amp = amp.as<T>();
+    a.scale = static_cast<T>(1.0 / static_cast<double>(S));
+    return a;
+  }
+
+  GatherArgs<T> gather_args(int mode) const {
+    GatherArgs<T> g;
+    g.mode = mode;
+    g.ntiles = L.ntiles();
+    g.tile_h = L.tile_h;
+    g.tiles = tiles.as<int4>();
+    g.tile_frames = tile_frames.as<int32_t>();
+    g.fr_r = fr_r.as<int32_t>();
+    g.fr_c = fr_c.as<int32_t>();
+    g.fr_sub = fr_sub.as<int32_t>();
+    g.S = S;
+    g.sub_off = sub_off.as<int64_t>();
+    g.sub_h = sub_h.as<int32_t>();
+    g.sub_w = sub_w.as<int32_t>();
+    g.sub_pbeg = sub_pbeg.as<int32_t>();
+    g.ps = psides.as<PairSide>();
+    return g;
+  }
+
+  // Per-subdomain R-factor numerators from rf_part (+ all-reduce over ranks).
+  void reduce_rf(bool gated) {
+    cudaStream_t s = st();
+    if (comm) PDD_CUDA(cudaMemsetAsync(rf_sub(), 0, sizeof(double) * D, s));
+    PDD_CUDA(launch_segsum(rf_part.as<double>(), 1, 0, sub_fr_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                           rf_sub(), gated ? skipA() : nullptr, s));
+    if (comm) comm->allreduce_sum_f64(rf_sub(), D, s);
+  }
+  void reduce_re() {
+    cudaStream_t s = st();
+    if (comm) PDD_CUDA(cudaMemsetAsync(diff_sub(), 0, sizeof(double) * 2 * D, s));
+    PDD_CUDA(launch_segsum(re_part.as<double>(), 2, 0, sub_tile_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                           diff_sub(), skipB(), s));
+    PDD_CUDA(launch_segsum(re_part.as<double>(), 2, 1, sub_tile_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                           norm_sub(), skipB(), s));
+    if (comm) comm->allreduce_sum_f64(diff_sub(), 2 * D, s);
+  }
+
+  // v = (s_1 + s_2)/2 with s_side = u_side + Lambda_side exchanged across ranks.
+  void consensus(const cx<T>* u, const cx<T>* lam, cx<T>* sbuf, cx<T>* v, const int* skip) {
+    cudaStream_t s = st();
+    const int np = static_cast<int>(L.lpairs.size());
+    PDD_CUDA(launch_pack<T>(pgeom.as<PairGeom>(), np, L.max_pair_pix, u, lam, sbuf, skip, s));
+    if (comm && !L.exch.empty()) {
+      comm->group_start();
+      for (const auto& e : L.exch) {
+        const PairGeom& pg = L.pgeom[e.lp];
+        const int64_t n = static_cast<int64_t>(pg.h) * pg.w;
+        comm->send(sbuf + pg.s_off + e.my_side * n, sizeof(cx<T>) * n, e.peer, s);
+        comm->recv(sbuf + pg.s_off + (1 - e.my_side) * n, sizeof(cx<T>) * n, e.peer, s);
+      }
+      comm->group_end();
+    }
+    PDD_CUDA(launch_vstep<T>(pgeom.as<PairGeom>(), np, L.max_pair_pix, sbuf, v, skip, s));
+  }
+
+  StateLayout state_layout(const Plan& plan) const {
+    StateLayout sl;
+    sl.local_subs = L.local_subs;
+    for (int ld = 0; ld < L.nls(); ++ld) {
+      sl.sub_h.push_back(L.sub_h[ld]);
+      sl.sub_w.push_back(L.sub_w[ld]);
+      sl.sub_frames.push_back(L.sub_fr_beg[ld + 1] - L.sub_fr_beg[ld]);
+    }
+    sl.local_pairs = L.lpairs;
+    for (const auto& pg : L.pgeom) {
+      sl.pair_h.push_back(pg.h);
+      sl.pair_w.push_back(pg.w);
+    }
+    sl.S = S;
+    return sl;
+  }
+
+  void reset_ctl(int iter, int max_iters, int rule, double tol_rf, double tol_re) {
+    RunCtl c{};
+    c.iter = iter;
+    c.max_iters = max_iters;
+    c.rule = rule;
+    c.tol_rf = tol_rf;
+    c.tol_re = tol_re;
+    c.l1 = l1;
+    c.rec_cap = rec_cap;
+    PDD_CUDA(cudaMemcpyAsync(ctl.get(), &c, sizeof(c), cudaMemcpyHostToDevice, st()));
+    PDD_CUDA(cudaStreamSynchronize(st()));
+  }
+  RunCtl read_ctl() {
+    RunCtl c{};
+    PDD_CUDA(cudaMemcpyAsync(&c, ctl.get(), sizeof(c), cudaMemcpyDeviceToHost, st()));
+    PDD_CUDA(cudaStreamSynchronize(st()));
+    return c;
+  }
+};
+
+}  // namespace pdd

@@ -1,0 +1,134 @@
+// Small RAII helpers for device memory, streams and graphs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace pdd {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define PDD_CUDA(call) ::pdd::cuda_check((call), #call)
+
+// Untyped device allocation.  Freed on destruction.
+class DevMem {
+ public:
+  DevMem() = default;
+  explicit DevMem(size_t bytes) { alloc(bytes); }
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
+  DevMem& operator=(DevMem&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      n_ = o.n_;
+      o.p_ = nullptr;
+      o.n_ = 0;
+    }
+    return *this;
+  }
+  ~DevMem() { release(); }
+  void alloc(size_t bytes) {
+    release();
+    if (bytes == 0) return;
+    PDD_CUDA(cudaMalloc(&p_, bytes));
+    n_ = bytes;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p_);
+  }
+  void* get() const { return p_; }
+  size_t bytes() const { return n_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+template <typename U>
+DevMem upload(const std::vector<U>& v, cudaStream_t st) {
+  DevMem m(sizeof(U) * (v.empty() ? 1 : v.size()));
+  if (!v.empty()) PDD_CUDA(cudaMemcpyAsync(m.get(), v.data(), sizeof(U) * v.size(), cudaMemcpyHostToDevice, st));
+  return m;
+}
+
+class Stream {
+ public:
+  Stream() { PDD_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking)); }
+  ~Stream() {
+    if (s_) cudaStreamDestroy(s_);
+  }
+  Stream(const Stream&) = delete;
+  Stream& operator=(const Stream&) = delete;
+  cudaStream_t get() const { return s_; }
+  void sync() const { PDD_CUDA(cudaStreamSynchronize(s_)); }
+
+ private:
+  cudaStream_t s_ = nullptr;
+};
+
+class Graph {
+ public:
+  Graph() = default;
+  ~Graph() { reset(); }
+  Graph(const Graph&) = delete;
+  Graph& operator=(const Graph&) = delete;
+  void reset() {
+    if (exec_) cudaGraphExecDestroy(exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    exec_ = nullptr;
+    graph_ = nullptr;
+  }
+  bool ready() const { return exec_ != nullptr; }
+  template <class F>
+  void capture(cudaStream_t st, F&& body) {
+    reset();
+    PDD_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    PDD_CUDA(cudaStreamEndCapture(st, &graph_));
+    PDD_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
+  }
+  void launch(cudaStream_t st) const { PDD_CUDA(cudaGraphLaunch(exec_, st)); }
+
+ private:
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t exec_ = nullptr;
+};
+
+// Scoped device selection.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    PDD_CUDA(cudaGetDevice(&prev_));
+    if (dev != prev_) PDD_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev_); }
+
+ private:
+  int prev_ = 0;
+};
+
+}  // namespace pdd

@@ -1,0 +1,256 @@
+// Per-frame fused kernel: the data-parallel heart of the OD²P iteration.
+//
+// One frame per Fft2<T,S,R>::NT threads, FPB frames per CTA.  Modes:
+//   FWD    : patch gather S_j u (field.cpp:5-16) x probe -> FFT2 -> A u
+//            (forward.cpp:28-41); optional outputs: frames, intensities
+//            (forward.cpp:95-106), per-frame R-factor partials
+//            sum | |A u| - sqrt f | (solver.cpp:207-214).
+//   ADJ    : frames -> IFFT2 -> x conj(probe) (forward.cpp:43-54 minus the
+//            overlap-add, which the deterministic gather kernel does).
+//   SWEEP  : the nonblind z/Gamma step (solver.cpp:125-139) fused between the
+//            two transforms: y = Gamma + A u, z = prox(y) (stagm.cpp:45-73),
+//            Gamma' = y - z, then resid = z - Gamma' -> IFFT2 -> x conj(P)
+//            (solver.cpp:157-164).  R-factor partials of u^n ride along.
+//   BLIND  : like SWEEP with the subdomain probe copy W_d (blind.cpp:224-242);
+//            additionally keeps q_j = IFFT2(resid) (the probe update needs it
+//            before conj(W^{n+1}) is known) and the shared-probe R-factor of
+//            u^n via a second forward transform (blind.cpp:320-332).
+#pragma once
+
+#include "fft.cuh"
+
+namespace pdd {
+
+enum FrameMode : int { kFwd = 1, kAdj = 2, kSweep = 3, kBlind = 4 };
+
+template <typename T>
+struct FrameArgs {
+  int nframes = 0;
+  const cx<T>* probe = nullptr;       // [S][S] (or per-frame probes via probe_idx)
+  const int32_t* probe_idx = nullptr; // optional [nframes] -> index into probe tiles (blind: subdomain copy)
+  const cx<T>* probe2 = nullptr;      // blind: shared probe w for the R-factor transform
+  const cx<T>* tw = nullptr;          // [S] W_S^k forward twiddles
+  const cx<T>* img = nullptr;         // concatenated images
+  const int64_t* off = nullptr;       // [nframes] element offset of window corner
+  const int32_t* pitch = nullptr;     // [nframes] image row pitch (elements)
+  const cx<T>* frames_in = nullptr;   // ADJ input [nframes][S][S]
+  cx<T>* frames_out = nullptr;        // FWD output A u
+  T* inten_out = nullptr;             // FWD |A u|^2
+  const T* amp = nullptr;             // sqrt(f)  [nframes][S][S]
+  const cx<T>* gamma_in = nullptr;
+  cx<T>* gamma_out = nullptr;
+  cx<T>* z_out = nullptr;             // diagnostic z (SWEEP/BLIND)
+  cx<T>* bp_out = nullptr;            // conj(P) . IFFT(.)  (ADJ/SWEEP) or q_j = IFFT(resid) (BLIND)
+  double* rf_part = nullptr;          // [nframes]
+  const int* stop_flag = nullptr;     // if non-null and *stop_flag != 0: skip (device-side early stop)
+  T lam = T(0), eps = T(0.5);
+  int fast_prox = 1;
+  T scale = T(1);                     // 1/S (unitary normalisation per transform)
+};
+
+// ST-AGM per-pixel prox, stagm.cpp:45-73.  amp = sqrt(b).  The fast form is
+// exact whenever lam <= (1-eps)/eps: then the outer candidate never falls
+// below eps*sqrt(b) and neither the origin nor the inner point can win
+// (SURVEY.md sec. 0 item 3); the host selects it from (lam, eps).
+template <typename T>
+__device__ __forceinline__ T mag_obj(T m, T absy, T b, T root_b, T lam, T eps) {
+  T g;
+  if (m < eps * root_b) {
+    g = T(0.5) * (T(1) - eps) * (b - m * m / eps);
+  } else {
+    const T d = m - root_b;
+    g = T(0.5) * d * d;
+  }
+  const T e = m - absy;
+  return g + T(0.5) * lam * e * e;
+}
+
+template <typename T>
+__device__ __forceinline__ cx<T> stagm_prox(cx<T> y, T amp, T lam, T eps, bool fast) {
+  const T absy = sqrt(norm2(y));
+  T m = (amp + lam * absy) / (T(1) + lam);
+  if (!fast) {
+    const T b = amp * amp, inner_edge = eps * amp;
+    if (m < inner_edge) m = inner_edge;
+    T best = mag_obj(m, absy, b, amp, lam, eps);
+    const T o0 = mag_obj(T(0), absy, b, amp, lam, eps);
+    if (o0 < best) {
+      best = o0;
+      m = T(0);
+    }
+    const T ic = lam - (T(1) - eps) / eps;
+    if (ic > T(0)) {
+      const T mi = lam * absy / ic;
+      if (mi < inner_edge) {
+        const T oi = mag_obj(mi, absy, b, amp, lam, eps);
+        if (oi < best) m = mi;
+      }
+    }
+  }
+  if (absy > T(0)) return cx<T>{y.x / absy * m, y.y / absy * m};
+  return cx<T>{m, T(0)};
+}
+
+// Sum a per-thread double over the NT threads of one frame slot; result valid
+// in the slot's thread 0.  Fixed shuffle tree => deterministic.
+template <int NT>
+__device__ __forceinline__ double slot_sum(double v, double* red, int t, int slot) {
+  if constexpr (NT <= 32) {
+#pragma unroll
+    for (int o = NT / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o, NT);
+    return v;
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    constexpr int NW = NT / 32;
+    if ((t & 31) == 0) red[slot * NW + t / 32] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (t == 0)
+      for (int w = 0; w < NW; ++w) s += red[slot * NW + w];
+    return s;
+  }
+}
+
+template <typename T, int S, int R, int FPB, int MODE>
+__global__ void __launch_bounds__(Fft2<T, S, R>::NT* FPB)
+    frame_kernel(const FrameArgs<T> a) {
+  using E = Fft2<T, S, R>;
+  constexpr int G = E::G, NT = E::NT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* tws = reinterpret_cast<cx<T>*>(smem_raw);
+  cx<T>* bufs = tws + S;
+  double* red = reinterpret_cast<double*>(bufs + FPB * E::TILE);
+
+  if (a.stop_flag && *a.stop_flag) return;  // uniform across the grid
+
+  const int tid = threadIdx.x;
+  const int slot = tid / NT, t = tid % NT;
+  cx<T>* buf = bufs + slot * E::TILE;
+  for (int i = tid; i < S; i += NT * FPB) tws[i] = a.tw[i];
+  const int f = blockIdx.x * FPB + slot;
+  const bool live = f < a.nframes;
+  __syncthreads();
+
+  cx<T> v[R];
+  const int y = t / G, g = t % G;      // row layout
+  const int x = t % S, c = t / S;      // Fourier layout
+  const int64_t fbase = static_cast<int64_t>(f) * S * S;
+
+  const cx<T>* probe = a.probe;
+  if (a.probe_idx && live) probe = a.probe + static_cast<int64_t>(a.probe_idx[f]) * S * S;
+
+  double rf = 0.0;
+  if constexpr (MODE != kAdj) {
+    cx<T> patch[MODE == kBlind ? R : 1];
+    if (live) {
+      const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
+      const cx<T>* pr = probe + y * S + g;
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const cx<T> u = src[G * m];
+        if constexpr (MODE == kBlind) patch[m] = u;
+        v[m] = u * pr[G * m];
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = cx<T>{T(0), T(0)};
+    }
+
+    if constexpr (MODE == kBlind) {
+      // Shared-probe forward transform for the lagged R-factor of u^n.
+      cx<T> w2[R];
+      const cx<T>* pr2 = a.probe2 + y * S + g;
+#pragma unroll
+      for (int m = 0; m < R; ++m) w2[m] = patch[m] * pr2[G * m];
+      E::forward(w2, buf, tws, t);
+      if (live && a.rf_part) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < R / G; ++q)
+#pragma unroll
+          for (int k1 = 0; k1 < G; ++k1) {
+            const int ky = c + G * q + R * k1;
+            const cx<T> au = w2[q * G + k1] * a.scale;
+            acc += fabs(sqrt(norm2(au)) - a.amp[fbase + ky * S + x]);
+          }
+        rf = static_cast<double>(acc);
+      }
+      __syncthreads();
+    }
+
+    E::forward(v, buf, tws, t);
+
+    if (live) {
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < R / G; ++q) {
+        // Compiler fence per chunk of G elements: bounds the number of
+        // Gamma/amp loads in flight (and so live registers) without giving
+        // up the G-wide memory-level parallelism.
+        if constexpr (MODE != kFwd) asm volatile("" ::: "memory");
+#pragma unroll
+        for (int k1 = 0; k1 < G; ++k1) {
+          const int ky = c + G * q + R * k1;
+          const int64_t idx = fbase + ky * S + x;
+          const cx<T> au = v[q * G + k1] * a.scale;
+          if constexpr (MODE == kFwd) {
+            if (a.frames_out) a.frames_out[idx] = au;
+            if (a.inten_out) a.inten_out[idx] = norm2(au);
+            if (a.rf_part) acc += fabs(sqrt(norm2(au)) - a.amp[idx]);
+          } else {
+            const T am = a.amp[idx];
+            if constexpr (MODE == kSweep) acc += fabs(sqrt(norm2(au)) - am);
+            const cx<T> yv = a.gamma_in[idx] + au;
+            const cx<T> z = stagm_prox(yv, am, a.lam, a.eps, a.fast_prox != 0);
+            const cx<T> gn = yv - z;
+            a.gamma_out[idx] = gn;
+            if (a.z_out) a.z_out[idx] = z;
+            v[q * G + k1] = z - gn;
+          }
+        }
+      }
+      if constexpr (MODE != kBlind) rf = static_cast<double>(acc);
+    } else if constexpr (MODE != kFwd) {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = cx<T>{T(0), T(0)};
+    }
+  } else {
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < R / G; ++q)
+#pragma unroll
+        for (int k1 = 0; k1 < G; ++k1) {
+          const int ky = c + G * q + R * k1;
+          v[q * G + k1] = a.frames_in[fbase + ky * S + x];
+        }
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = cx<T>{T(0), T(0)};
+    }
+  }
+
+  if constexpr (MODE != kFwd) {
+    E::inverse(v, buf, tws, t);
+    if (live) {
+      cx<T>* dst = a.bp_out + fbase + y * S + g;
+      const cx<T>* pr = probe + y * S + g;
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const cx<T> q = v[m] * a.scale;
+        // BLIND keeps q_j itself: conj(W^{n+1}) is applied in the gather.
+        if constexpr (MODE == kBlind) dst[G * m] = q;
+        else dst[G * m] = mul_conj(q, pr[G * m]);
+      }
+    }
+  }
+
+  if constexpr (MODE != kAdj) {
+    if (a.rf_part) {
+      const double s = slot_sum<NT>(rf, red, t, slot);
+      if (t == 0 && live) a.rf_part[f] = s;
+    }
+  }
+}
+
+}  // namespace pdd

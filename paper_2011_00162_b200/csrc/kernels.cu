@@ -1,0 +1,487 @@
+// CUDA kernels of the OD²P iteration (sm_100a) and their launchers.
+//
+// frame_kernel (frame_kernel.cuh) carries the FFT-bound per-frame work; the
+// kernels here are the HBM-bound image-side passes:
+//   gather_kernel : deterministic overlap-add, i.e. the embed_add loop of
+//                   adjoint (forward.cpp:43-54) in gather form -- every output
+//                   pixel sums its covering frames in ascending frame index,
+//                   the reference's accumulation order -- fused with the
+//                   u-update, the Lambda-update and the RE partials of
+//                   solver.cpp:154-193 (or blind.cpp:253-277).
+//   pack / vstep  : the overlap consensus v = (s_1 + s_2)/2 with
+//                   s_side = u_side|overlap + Lambda_side (solver.cpp:141-151);
+//                   packing s separately is what makes the multi-GPU exchange a
+//                   single send/recv of s per pair.
+//   segsum        : fixed-shape reductions of per-frame / per-tile partials
+//                   (bit-identical for any GPU count at fixed D).
+#include <cuda_runtime.h>
+
+#include "frame_kernel.cuh"
+#include "kernels.hpp"
+
+namespace pdd {
+
+// ---------------------------------------------------------------------------
+// frame kernel dispatch
+template <typename T, int S>
+struct FrameCfg;
+// float: whole rows in registers up to S = 32; two-level rows beyond.
+template <> struct FrameCfg<float, 2> { static constexpr int R = 2, FPB = 64; };
+template <> struct FrameCfg<float, 4> { static constexpr int R = 4, FPB = 32; };
+template <> struct FrameCfg<float, 8> { static constexpr int R = 8, FPB = 16; };
+template <> struct FrameCfg<float, 16> { static constexpr int R = 16, FPB = 8; };
+template <> struct FrameCfg<float, 32> { static constexpr int R = 32, FPB = 4; };
+template <> struct FrameCfg<float, 64> { static constexpr int R = 16, FPB = 1; };
+template <> struct FrameCfg<float, 128> { static constexpr int R = 32, FPB = 1; };
+template <> struct FrameCfg<double, 2> { static constexpr int R = 2, FPB = 64; };
+template <> struct FrameCfg<double, 4> { static constexpr int R = 4, FPB = 32; };
+template <> struct FrameCfg<double, 8> { static constexpr int R = 8, FPB = 16; };
+template <> struct FrameCfg<double, 16> { static constexpr int R = 16, FPB = 8; };
+template <> struct FrameCfg<double, 32> { static constexpr int R = 16, FPB = 2; };
+template <> struct FrameCfg<double, 64> { static constexpr int R = 16, FPB = 1; };
+
+template <typename T, int S, int MODE>
+static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
+  using C = FrameCfg<T, S>;
+  using E = Fft2<T, S, C::R>;
+  constexpr int threads = E::NT * C::FPB;
+  constexpr int nw = (E::NT + 31) / 32;
+  const size_t smem = sizeof(cx<T>) * (S + static_cast<size_t>(C::FPB) * E::TILE) + sizeof(double) * C::FPB * nw;
+  auto kern = frame_kernel<T, S, C::R, C::FPB, MODE>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (a.nframes <= 0) return cudaSuccess;
+  const int grid = (a.nframes + C::FPB - 1) / C::FPB;
+  kern<<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, int S>
+static cudaError_t launch_frame_mode(int mode, const FrameArgs<T>& a, cudaStream_t st) {
+  switch (mode) {
+    case kFwd: return launch_frame_s<T, S, kFwd>(a, st);
+    case kAdj: return launch_frame_s<T, S, kAdj>(a, st);
+    case kSweep: return launch_frame_s<T, S, kSweep>(a, st);
+    case kBlind: return launch_frame_s<T, S, kBlind>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <>
+bool frame_supported<float>(int S) {
+  return S == 2 || S == 4 || S == 8 || S == 16 || S == 32 || S == 64 || S == 128;
+}
+template <>
+bool frame_supported<double>(int S) {
+  return S == 2 || S == 4 || S == 8 || S == 16 || S == 32 || S == 64;
+}
+
+template <>
+cudaError_t launch_frame<float>(int mode, int S, const FrameArgs<float>& a, cudaStream_t st) {
+  switch (S) {
+    case 2: return launch_frame_mode<float, 2>(mode, a, st);
+    case 4: return launch_frame_mode<float, 4>(mode, a, st);
+    case 8: return launch_frame_mode<float, 8>(mode, a, st);
+    case 16: return launch_frame_mode<float, 16>(mode, a, st);
+    case 32: return launch_frame_mode<float, 32>(mode, a, st);
+    case 64: return launch_frame_mode<float, 64>(mode, a, st);
+    case 128: return launch_frame_mode<float, 128>(mode, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+template <>
+cudaError_t launch_frame<double>(int mode, int S, const FrameArgs<double>& a, cudaStream_t st) {
+  switch (S) {
+    case 2: return launch_frame_mode<double, 2>(mode, a, st);
+    case 4: return launch_frame_mode<double, 4>(mode, a, st);
+    case 8: return launch_frame_mode<double, 8>(mode, a, st);
+    case 16: return launch_frame_mode<double, 16>(mode, a, st);
+    case 32: return launch_frame_mode<double, 32>(mode, a, st);
+    case 64: return launch_frame_mode<double, 64>(mode, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------------------
+// block reduction of two doubles, fixed tree; result in thread 0.
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* sm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sm[2 * w] = a;
+    sm[2 * w + 1] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    a = 0.0;
+    b = 0.0;
+    for (int i = 0; i < nw; ++i) {
+      a += sm[2 * i];
+      b += sm[2 * i + 1];
+    }
+  }
+}
+
+constexpr int kMaxRowsPerThread = 4;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
+  __shared__ double sm[16];
+  if (a.stop_flag && *a.stop_flag) return;
+  const int4 td = a.tiles[blockIdx.x];
+  const int sub = td.x, tr0 = td.y, tc0 = td.z, fb = td.w, fe = a.tiles[blockIdx.x + 1].w;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int H = a.sub_h[sub], W = a.sub_w[sub];
+  const int c = tc0 + tx;
+  const int nrow = a.tile_h >> 3;
+  const int S = a.S;
+  const int64_t SS = static_cast<int64_t>(S) * S;
+
+  cx<T> acc[kMaxRowsPerThread];
+  T wacc[kMaxRowsPerThread];
+  double dacc[kMaxRowsPerThread];
+#pragma unroll
+  for (int i = 0; i < kMaxRowsPerThread; ++i) {
+    acc[i] = cx<T>{T(0), T(0)};
+    wacc[i] = T(0);
+    dacc[i] = 0.0;
+  }
+
+  for (int k = fb; k < fe; ++k) {
+    const int fr = a.tile_frames[k];
+    const int cc = c - a.fr_c[fr];
+    if (cc < 0 || cc >= S) continue;
+    const int r0 = a.fr_r[fr];
+#pragma unroll
+    for (int i = 0; i < kMaxRowsPerThread; ++i) {
+      if (i >= nrow) break;
+      const int rr = tr0 + ty + 8 * i - r0;
+      if (rr < 0 || rr >= S) continue;
+      const int64_t pix = static_cast<int64_t>(rr) * S + cc;
+      if (a.mode == kGatherDensity) {
+        dacc[i] += static_cast<double>(norm2(a.probe[pix]));
+      } else if (a.mode == kGatherBlind) {
+        const cx<T> w = a.probe[static_cast<int64_t>(sub) * SS + pix];
+        acc[i] += mul_conj(a.bp[fr * SS + pix], w);
+        wacc[i] += norm2(w);
+      } else {
+        acc[i] += a.bp[fr * SS + pix];
+      }
+    }
+  }
+
+  double diff = 0.0, nrm = 0.0;
+  const int64_t base = a.sub_off[sub];
+#pragma unroll
+  for (int i = 0; i < kMaxRowsPerThread; ++i) {
+    if (i >= nrow) break;
+    const int r = tr0 + ty + 8 * i;
+    if (r >= H || c >= W) continue;
+    const int64_t pi = base + static_cast<int64_t>(r) * W + c;
+    if (a.mode == kGatherAdjoint) {
+      a.out[pi] = acc[i];
+      continue;
+    }
+    if (a.mode == kGatherDensity) {
+      a.dens_out[pi] = dacc[i];
+      continue;
+    }
+    cx<T> num = acc[i] * a.eta;
+    const int pb = a.sub_pbeg[sub], pe = a.sub_pbeg[sub + 1];
+    for (int q = pb; q < pe; ++q) {
+      const PairSide p = a.ps[q];
+      if (r < p.r0 || r >= p.r1 || c < p.c0 || c >= p.c1) continue;
+      const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (c - p.c0);
+      num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
+    }
+    const cx<T> uo = a.u[pi];
+    cx<T> un;
+    if (a.mode == kGatherNonblind) {
+      const T d = a.denom[pi];
+      un = d < T(0) ? cx<T>{T(1), T(0)} : cx<T>{num.x / d, num.y / d};
+    } else {
+      const T rp = a.rpen[pi];
+      const T dd = a.eta * wacc[i] + rp + a.gamma;
+      const cx<T> nn = num + uo * a.gamma;
+      un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
+    }
+    for (int q = pb; q < pe; ++q) {
+      const PairSide p = a.ps[q];
+      if (r < p.r0 || r >= p.r1 || c < p.c0 || c >= p.c1) continue;
+      const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (c - p.c0);
+      a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
+    }
+    a.u[pi] = un;
+    const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);
+    const double dy = static_cast<double>(un.y) - static_cast<double>(uo.y);
+    diff += dx * dx + dy * dy;
+    nrm += static_cast<double>(un.x) * un.x + static_cast<double>(un.y) * un.y;
+  }
+  if (a.re_part) {
+    block_sum2(diff, nrm, sm);
+    if (threadIdx.x == 0) {
+      a.re_part[2 * blockIdx.x] = diff;
+      a.re_part[2 * blockIdx.x + 1] = nrm;
+    }
+  }
+}
+
+template <typename T>
+cudaError_t launch_gather(const GatherArgs<T>& a, cudaStream_t st) {
+  if (a.ntiles <= 0) return cudaSuccess;
+  if (a.tile_h < 8 || a.tile_h > 8 * kMaxRowsPerThread || a.tile_h % 8) return cudaErrorInvalidValue;
+  gather_kernel<T><<<a.ntiles, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void pack_kernel(const PairGeom* pairs, const cx<T>* u, const cx<T>* lam, cx<T>* s,
+                            const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  const PairGeom p = pairs[blockIdx.y];
+  const int n = p.h * p.w;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int rr = i / p.w, cc = i % p.w;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      if (p.u_off[side] < 0) continue;
+      s[p.s_off + static_cast<int64_t>(side) * n + i] =
+          u[p.u_off[side] + static_cast<int64_t>(rr) * p.u_pitch[side] + cc] + lam[p.lam_off[side] + i];
+    }
+  }
+}
+
+template <typename T>
+__global__ void vstep_kernel(const PairGeom* pairs, const cx<T>* s, cx<T>* v, const int* stop_flag) {
+  if (stop_flag && *stop_flag) return;
+  const PairGeom p = pairs[blockIdx.y];
+  const int n = p.h * p.w;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[p.v_off + i] = (s[p.s_off + i] + s[p.s_off + n + i]) * T(0.5);
+}
+
+template <typename T>
+cudaError_t launch_pack(const PairGeom* pairs, int npairs, int maxpix, const cx<T>* u, const cx<T>* lam,
+                        cx<T>* s, const int* stop_flag, cudaStream_t st) {
+  if (npairs <= 0) return cudaSuccess;
+  dim3 grid(std::min((maxpix + 255) / 256, 1184), npairs);
+  pack_kernel<T><<<grid, 256, 0, st>>>(pairs, u, lam, s, stop_flag);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_vstep(const PairGeom* pairs, int npairs, int maxpix, const cx<T>* s, cx<T>* v,
+                         const int* stop_flag, cudaStream_t st) {
+  if (npairs <= 0) return cudaSuccess;
+  dim3 grid(std::min((maxpix + 255) / 256, 1184), npairs);
+  vstep_kernel<T><<<grid, 256, 0, st>>>(pairs, s, v, stop_flag);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void fill_kernel(cx<T>* p, int64_t n, cx<T> value) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = value;
+}
+template <typename T>
+cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  fill_kernel<T><<<grid, 256, 0, st>>>(p, n, value);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+__global__ void segsum_kernel(const double* in, int stride, int comp, const int64_t* beg, const int* map,
+                              double* out, const int* skip) {
+  __shared__ double sm[16];
+  if (skip && *skip) return;
+  const int64_t b = beg[blockIdx.x], e = beg[blockIdx.x + 1];
+  double acc = 0.0, dummy = 0.0;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) acc += in[i * stride + comp];
+  block_sum2(acc, dummy, sm);
+  if (threadIdx.x == 0) out[map ? map[blockIdx.x] : blockIdx.x] = acc;
+}
+cudaError_t launch_segsum(const double* in, int stride, int comp, const int64_t* beg, int nseg, const int* map,
+                          double* out, const int* skip, cudaStream_t st) {
+  if (nseg <= 0) return cudaSuccess;
+  segsum_kernel<<<nseg, 256, 0, st>>>(in, stride, comp, beg, map, out, skip);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void frame_sums_kernel(const T* amp, int64_t per, double* out) {
+  __shared__ double sm[16];
+  const T* p = amp + blockIdx.x * per;
+  double acc = 0.0, dummy = 0.0;
+  for (int64_t i = threadIdx.x; i < per; i += blockDim.x) acc += static_cast<double>(p[i]);
+  block_sum2(acc, dummy, sm);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+template <typename T>
+cudaError_t launch_frame_sums(const T* amp, int64_t nfr, int64_t per, double* out, cudaStream_t st) {
+  if (nfr <= 0) return cudaSuccess;
+  frame_sums_kernel<T><<<static_cast<unsigned>(nfr), 256, 0, st>>>(amp, per, out);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void convert_amp_kernel(const void* src, int kind, T* amp, int64_t n, unsigned long long* neg) {
+  unsigned long long bad = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = kind == 1 ? static_cast<double>(static_cast<const float*>(src)[i]) : static_cast<const double*>(src)[i];
+    if (v < 0.0) {
+      ++bad;
+      v = 0.0;
+    }
+    amp[i] = static_cast<T>(kind == 0 ? sqrt(v) : v);
+  }
+  if (bad && neg) atomicAdd(neg, bad);
+}
+template <typename T>
+cudaError_t launch_convert_amp(const void* src, int kind, T* amp, int64_t n, unsigned long long* neg,
+                               cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  convert_amp_kernel<T><<<grid, 256, 0, st>>>(src, kind, amp, n, neg);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void denom_sub_kernel(const double* dens, const uint8_t* pin, const PairSide* ps, int nps, int H, int W,
+                                 T eta, T r, T* denom, unsigned long long* bad, int blind) {
+  const int64_t n = static_cast<int64_t>(H) * W;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int rr = static_cast<int>(i / W), cc = static_cast<int>(i % W);
+    double d = blind ? 0.0 : static_cast<double>(eta) * dens[i];
+    for (int k = 0; k < nps; ++k) {
+      const PairSide p = ps[k];
+      if (rr >= p.r0 && rr < p.r1 && cc >= p.c0 && cc < p.c1) d += static_cast<double>(r);
+    }
+    if (!blind && !pin[i] && dens[i] <= 0.0) atomicAdd(bad, 1ull);
+    denom[i] = pin[i] ? T(-1) : static_cast<T>(d);
+  }
+}
+template <typename T>
+cudaError_t launch_denom_sub(const double* dens, const uint8_t* pin, const PairSide* ps, int nps, int H, int W,
+                             T eta, T r, T* denom, unsigned long long* bad, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(H) * W;
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  denom_sub_kernel<T><<<grid, 256, 0, st>>>(dens, pin, ps, nps, H, W, eta, r, denom, bad, 0);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_rpen_sub(const uint8_t* pin, const PairSide* ps, int nps, int H, int W, T r, T* rpen,
+                            cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(H) * W;
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  denom_sub_kernel<T><<<grid, 256, 0, st>>>(nullptr, pin, ps, nps, H, W, T(0), r, rpen, nullptr, 1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// iteration control: stop rules of run() (solver.cpp:225-262) on the device
+__global__ void gate_kernel(RunCtl* c) {
+  c->skipA = !(c->stop == 0 || (c->stop == c->iter && !c->done));
+  c->skipB = c->stop != 0;
+}
+__global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, double* rec) {
+  if (c->skipA) return;
+  double s = 0.0;
+  for (int d = 0; d < D; ++d) s += rf_sub[d];
+  const double rf = s / c->l1;
+  const int n = c->iter;
+  if (n >= 1) {
+    rec[2 * ((n - 1) % c->rec_cap)] = rf;
+    if (c->stop == n) {
+      c->done = 1;
+    } else if (!isfinite(rf)) {
+      c->diverged = n;
+      c->stop = n;
+      c->done = 1;
+    } else if (c->rule == 0 && rf <= c->tol_rf) {
+      c->stop = n;
+      c->done = 1;
+    }
+  }
+  c->skipB = c->stop != 0;
+}
+__global__ void re_finalize_kernel(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
+  if (c->skipB) return;
+  double re = 0.0;
+  bool finite = true;
+  for (int d = 0; d < D; ++d) {
+    const double e = sqrt(diff[d]) / sqrt(norm[d]);
+    if (!isfinite(e)) finite = false;
+    re = e > re ? e : re;
+  }
+  const int n = c->iter + 1;
+  rec[2 * ((n - 1) % c->rec_cap) + 1] = finite ? re : NAN;
+  c->iter = n;
+  if (!finite) {
+    c->diverged = n;
+    c->stop = n;
+  } else if (c->rule == 1 && re <= c->tol_re) {
+    c->stop = n;
+  } else if (n >= c->max_iters) {
+    c->stop = n;
+  }
+}
+cudaError_t launch_gate(RunCtl* c, cudaStream_t st) {
+  gate_kernel<<<1, 1, 0, st>>>(c);
+  return cudaGetLastError();
+}
+cudaError_t launch_rf_finalize(RunCtl* c, const double* rf_sub, int D, double* rec, cudaStream_t st) {
+  rf_finalize_kernel<<<1, 1, 0, st>>>(c, rf_sub, D, rec);
+  return cudaGetLastError();
+}
+cudaError_t launch_re_finalize(RunCtl* c, const double* diff, const double* norm, int D, double* rec,
+                               cudaStream_t st) {
+  re_finalize_kernel<<<1, 1, 0, st>>>(c, diff, norm, D, rec);
+  return cudaGetLastError();
+}
+
+// explicit instantiations
+template cudaError_t launch_gather<float>(const GatherArgs<float>&, cudaStream_t);
+template cudaError_t launch_gather<double>(const GatherArgs<double>&, cudaStream_t);
+template cudaError_t launch_pack<float>(const PairGeom*, int, int, const cx<float>*, const cx<float>*, cx<float>*,
+                                        const int*, cudaStream_t);
+template cudaError_t launch_pack<double>(const PairGeom*, int, int, const cx<double>*, const cx<double>*,
+                                         cx<double>*, const int*, cudaStream_t);
+template cudaError_t launch_vstep<float>(const PairGeom*, int, int, const cx<float>*, cx<float>*, const int*,
+                                         cudaStream_t);
+template cudaError_t launch_vstep<double>(const PairGeom*, int, int, const cx<double>*, cx<double>*, const int*,
+                                          cudaStream_t);
+template cudaError_t launch_fill<float>(cx<float>*, int64_t, cx<float>, cudaStream_t);
+template cudaError_t launch_fill<double>(cx<double>*, int64_t, cx<double>, cudaStream_t);
+template cudaError_t launch_frame_sums<float>(const float*, int64_t, int64_t, double*, cudaStream_t);
+template cudaError_t launch_frame_sums<double>(const double*, int64_t, int64_t, double*, cudaStream_t);
+template cudaError_t launch_convert_amp<float>(const void*, int, float*, int64_t, unsigned long long*, cudaStream_t);
+template cudaError_t launch_convert_amp<double>(const void*, int, double*, int64_t, unsigned long long*,
+                                                cudaStream_t);
+template cudaError_t launch_denom_sub<float>(const double*, const uint8_t*, const PairSide*, int, int, int, float,
+                                             float, float*, unsigned long long*, cudaStream_t);
+template cudaError_t launch_denom_sub<double>(const double*, const uint8_t*, const PairSide*, int, int, int, double,
+                                              double, double*, unsigned long long*, cudaStream_t);
+template cudaError_t launch_rpen_sub<float>(const uint8_t*, const PairSide*, int, int, int, float, float*,
+                                            cudaStream_t);
+template cudaError_t launch_rpen_sub<double>(const uint8_t*, const PairSide*, int, int, int, double, double*,
+                                             cudaStream_t);
+
+}  // namespace pdd

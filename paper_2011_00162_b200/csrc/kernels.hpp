@@ -1,0 +1,134 @@
+// Host-side launch interface between the C++ drivers and the CUDA kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cx.cuh"
+
+namespace pdd {
+
+template <typename T>
+struct FrameArgs;
+
+// One rectangle of one overlap pair, seen from one side, in that side's
+// subdomain-local coordinates (ddplan.cpp:14-19).
+struct PairSide {
+  int32_t r0, r1, c0, c1;
+  int64_t v_off;    // element offset of v_p in the concatenated v buffer
+  int64_t lam_off;  // element offset of Lambda_{p,side}
+};
+
+enum GatherMode : int {
+  kGatherAdjoint = 0,  // out = sum_j bp_j (forward.cpp:43-54 overlap-add)
+  kGatherNonblind = 1, // u-update + Lambda-update + RE partials (solver.cpp:154-193)
+  kGatherBlind = 2,    // blind u-update with W^{n+1} (blind.cpp:253-272)
+  kGatherDensity = 3,  // rho = sum_j |P|^2 (forward.cpp:56-66), double
+};
+
+template <typename T>
+struct GatherArgs {
+  int mode = 0;
+  int ntiles = 0;
+  int tile_h = 8;                       // rows per tile (multiple of 8); width is 32
+  const int4* tiles = nullptr;          // {sub, r0, c0, frame_begin}; end = tiles[i+1].w
+  const int32_t* tile_frames = nullptr; // local frame ids, ascending j per tile
+  const int32_t* fr_r = nullptr;        // [nframes] window corner (subdomain coords)
+  const int32_t* fr_c = nullptr;
+  const int32_t* fr_sub = nullptr;      // [nframes] owning local subdomain
+  int S = 0;
+  const cx<T>* bp = nullptr;            // [nframes][S][S]
+  const cx<T>* probe = nullptr;         // density: P; blind: W copies [nsub][S][S]
+  const int64_t* sub_off = nullptr;     // [nsub] offset into image buffers
+  const int32_t* sub_h = nullptr;
+  const int32_t* sub_w = nullptr;
+  cx<T>* u = nullptr;
+  const T* denom = nullptr;             // nonblind: eta*rho + r*npairs (< 0: pinned)
+  const T* rpen = nullptr;              // blind: r*npairs (< 0: pinned)
+  const int32_t* sub_pbeg = nullptr;    // CSR over PairSide per subdomain (ascending p)
+  const PairSide* ps = nullptr;
+  const cx<T>* v = nullptr;
+  cx<T>* lam = nullptr;
+  T eta = T(0), r = T(0), gamma = T(0);
+  cx<T>* out = nullptr;                 // adjoint output (image layout)
+  double* dens_out = nullptr;           // density output (image layout)
+  double* re_part = nullptr;            // [ntiles][2] (diff, norm)
+  const int* stop_flag = nullptr;
+};
+
+// Overlap pair with both sides' image addressing (for v / s packing).
+struct PairGeom {
+  int32_t h, w;
+  int64_t u_off[2];    // element offset of the overlap's top-left in each side's image buffer (-1: remote side)
+  int32_t u_pitch[2];
+  int64_t v_off;       // offset into v (and into the s exchange buffers: s[side] = s_off + side*h*w)
+  int64_t lam_off[2];
+  int64_t s_off;
+};
+
+template <typename T>
+cudaError_t launch_frame(int mode, int S, const FrameArgs<T>& a, cudaStream_t st);
+template <typename T>
+bool frame_supported(int S);
+
+template <typename T>
+cudaError_t launch_gather(const GatherArgs<T>& a, cudaStream_t st);
+
+// s_{p,side} = u_side|overlap + Lambda_{p,side} for the sides present locally.
+template <typename T>
+cudaError_t launch_pack(const PairGeom* pairs, int npairs, int maxpix, const cx<T>* u, const cx<T>* lam,
+                        cx<T>* s, const int* stop_flag, cudaStream_t st);
+// v_p = 0.5 * (s_{p,0} + s_{p,1})
+template <typename T>
+cudaError_t launch_vstep(const PairGeom* pairs, int npairs, int maxpix, const cx<T>* s, cx<T>* v,
+                         const int* stop_flag, cudaStream_t st);
+
+template <typename T>
+cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st);
+
+// Deterministic segmented sums: out[map[s]] = sum_{i in [beg[s], beg[s+1])} in[i*stride+comp]
+// (fixed tree; map == nullptr means identity).  Skipped when *skip != 0.
+cudaError_t launch_segsum(const double* in, int stride, int comp, const int64_t* beg, int nseg, const int* map,
+                          double* out, const int* skip, cudaStream_t st);
+
+// Per-frame sums of amplitudes (for the R-factor denominator), double.
+template <typename T>
+cudaError_t launch_frame_sums(const T* amp, int64_t nfr, int64_t per, double* out, cudaStream_t st);
+
+// amp[i] = sqrt(src) (kind 0: f64 intensity) or src (kind 1: f32 amplitude, kind 2: f64 amplitude);
+// negative inputs are counted into *neg (FrameStack::validate, scan.cpp:46-56).
+template <typename T>
+cudaError_t launch_convert_amp(const void* src, int kind, T* amp, int64_t n, unsigned long long* neg,
+                               cudaStream_t st);
+
+// Denominators for one subdomain: d = eta*rho (+ r per covering pair side); pinned -> -1;
+// counts interior pixels with rho <= 0 into *bad.  (solver.cpp:53-75)
+template <typename T>
+cudaError_t launch_denom_sub(const double* dens, const uint8_t* pin, const PairSide* ps, int nps, int H, int W,
+                             T eta, T r, T* denom, unsigned long long* bad, cudaStream_t st);
+// Blind penalty: rpen = r per covering pair side, pinned -> -1 (blind.cpp:100-107).
+template <typename T>
+cudaError_t launch_rpen_sub(const uint8_t* pin, const PairSide* ps, int nps, int H, int W, T r, T* rpen,
+                            cudaStream_t st);
+
+// Iteration control (device-side stop logic; see nonblind.cpp).
+struct RunCtl {
+  int iter;      // completed iterations (state is u^iter)
+  int stop;      // 0 or the final iteration
+  int done;      // final R-factor recorded
+  int diverged;  // iteration at which a non-finite RF/RE appeared
+  int max_iters;
+  int rule;      // 0: R-factor, 1: relative error
+  int skipA;     // frame pass disabled
+  int skipB;     // update pass disabled
+  int rec_cap;   // records ring capacity (iterations)
+  int pad;
+  double tol_rf, tol_re, l1;
+};
+cudaError_t launch_gate(RunCtl* c, cudaStream_t st);
+cudaError_t launch_rf_finalize(RunCtl* c, const double* rf_sub, int D, double* rec, cudaStream_t st);
+cudaError_t launch_re_finalize(RunCtl* c, const double* diff, const double* norm, int D, double* rec,
+                               cudaStream_t st);
+
+}  // namespace pdd

@@ -1,0 +1,128 @@
+#include "layout.hpp"
+
+#include <algorithm>
+
+namespace pdd {
+
+Layout Layout::build(const Plan& plan, int rank, int world) {
+  Layout L;
+  L.D = plan.D;
+  L.rank = rank;
+  L.world = world;
+  L.S = static_cast<int>(plan.g.s);
+  L.sub_local.assign(plan.D, -1);
+  for (int d = 0; d < plan.D; ++d)
+    if (owner_of(d, plan.D, world) == rank) {
+      L.sub_local[d] = static_cast<int>(L.local_subs.size());
+      L.local_subs.push_back(d);
+    }
+
+  // images and frames
+  L.sub_fr_beg.push_back(0);
+  for (int ld = 0; ld < L.nls(); ++ld) {
+    const int d = L.local_subs[ld];
+    const Rect& sub = plan.subs[d];
+    L.sub_img_off.push_back(L.img_elems);
+    L.sub_h.push_back(static_cast<int32_t>(sub.h()));
+    L.sub_w.push_back(static_cast<int32_t>(sub.w()));
+    const Geometry& lg = plan.local[d];
+    for (int64_t k = 0; k < lg.J(); ++k) {
+      const int64_t r = lg.pos[2 * k], c = lg.pos[2 * k + 1];
+      L.fr_global.push_back(plan.frames_of[d][k]);
+      L.fr_off.push_back(L.img_elems + r * sub.w() + c);
+      L.fr_pitch.push_back(static_cast<int32_t>(sub.w()));
+      L.fr_r.push_back(static_cast<int32_t>(r));
+      L.fr_c.push_back(static_cast<int32_t>(c));
+      L.fr_sub.push_back(ld);
+    }
+    L.img_elems += sub.area();
+    L.sub_fr_beg.push_back(static_cast<int64_t>(L.fr_global.size()));
+  }
+  L.nfr = static_cast<int64_t>(L.fr_global.size());
+
+  // gather tiles: 32 wide, tile_h high; covering frames in ascending order
+  L.tile_h = L.img_elems >= (int64_t(4) << 20) ? 32 : 8;
+  const int th = L.tile_h, tw = 32;
+  L.sub_tile_beg.push_back(0);
+  for (int ld = 0; ld < L.nls(); ++ld) {
+    const int64_t H = L.sub_h[ld], W = L.sub_w[ld];
+    const int64_t ntr = (H + th - 1) / th, ntc = (W + tw - 1) / tw;
+    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(ntr * ntc));
+    for (int64_t f = L.sub_fr_beg[ld]; f < L.sub_fr_beg[ld + 1]; ++f) {
+      const int64_t r0 = L.fr_r[f], c0 = L.fr_c[f];
+      const int64_t tr_a = r0 / th, tr_b = std::min(ntr - 1, (r0 + L.S - 1) / th);
+      const int64_t tc_a = c0 / tw, tc_b = std::min(ntc - 1, (c0 + L.S - 1) / tw);
+      for (int64_t tr = tr_a; tr <= tr_b; ++tr)
+        for (int64_t tc = tc_a; tc <= tc_b; ++tc) lists[tr * ntc + tc].push_back(static_cast<int32_t>(f));
+    }
+    for (int64_t tr = 0; tr < ntr; ++tr)
+      for (int64_t tc = 0; tc < ntc; ++tc) {
+        const auto& l = lists[tr * ntc + tc];
+        L.tiles.push_back(int4{ld, static_cast<int>(tr * th), static_cast<int>(tc * tw),
+                               static_cast<int>(L.tile_frames.size())});
+        L.tile_frames.insert(L.tile_frames.end(), l.begin(), l.end());
+      }
+    L.sub_tile_beg.push_back(static_cast<int64_t>(L.tiles.size()));
+  }
+  L.tiles.push_back(int4{0, 0, 0, static_cast<int>(L.tile_frames.size())});
+
+  // overlap pairs touching a local subdomain, ascending global p
+  std::vector<int> lp_of(plan.overlaps.size(), -1);
+  for (size_t p = 0; p < plan.overlaps.size(); ++p) {
+    const auto& pr = plan.overlaps[p];
+    const int l1 = L.sub_local[pr.d1], l2 = L.sub_local[pr.d2];
+    if (l1 < 0 && l2 < 0) continue;
+    const int lp = static_cast<int>(L.lpairs.size());
+    lp_of[p] = lp;
+    L.lpairs.push_back(static_cast<int>(p));
+    PairGeom pg{};
+    pg.h = static_cast<int32_t>(pr.region.h());
+    pg.w = static_cast<int32_t>(pr.region.w());
+    const int64_t n = pr.region.area();
+    L.max_pair_pix = std::max<int>(L.max_pair_pix, static_cast<int>(n));
+    pg.v_off = L.v_elems;
+    pg.s_off = L.s_elems;
+    const int ds[2] = {pr.d1, pr.d2};
+    for (int side = 0; side < 2; ++side) {
+      const int ld = L.sub_local[ds[side]];
+      pg.lam_off[side] = L.lam_elems + side * n;
+      if (ld < 0) {
+        pg.u_off[side] = -1;
+        pg.u_pitch[side] = 0;
+      } else {
+        const Rect lo = plan.local_overlap(ds[side], p);
+        pg.u_off[side] = L.sub_img_off[ld] + lo.r0 * L.sub_w[ld] + lo.c0;
+        pg.u_pitch[side] = L.sub_w[ld];
+      }
+    }
+    if ((l1 < 0) != (l2 < 0)) {
+      const int my_side = l1 >= 0 ? 0 : 1;
+      L.exch.push_back(Exchange{lp, owner_of(ds[1 - my_side], plan.D, world), my_side});
+    }
+    L.v_elems += n;
+    L.lam_elems += 2 * n;
+    L.s_elems += 2 * n;
+    L.pgeom.push_back(pg);
+  }
+  L.sub_pbeg.push_back(0);
+  for (int ld = 0; ld < L.nls(); ++ld) {
+    const int d = L.local_subs[ld];
+    for (size_t p : plan.pairs_of(d)) {
+      const int lp = lp_of[p];
+      const int side = plan.overlaps[p].d1 == d ? 0 : 1;
+      const Rect lo = plan.local_overlap(d, p);
+      PairSide ps{};
+      ps.r0 = static_cast<int32_t>(lo.r0);
+      ps.r1 = static_cast<int32_t>(lo.r1);
+      ps.c0 = static_cast<int32_t>(lo.c0);
+      ps.c1 = static_cast<int32_t>(lo.c1);
+      ps.v_off = L.pgeom[lp].v_off;
+      ps.lam_off = L.pgeom[lp].lam_off[side];
+      L.psides.push_back(ps);
+    }
+    L.sub_pbeg.push_back(static_cast<int32_t>(L.psides.size()));
+  }
+  return L;
+}
+
+}  // namespace pdd

@@ -1,0 +1,65 @@
+// Device-side data layout of one rank's share of a decomposition plan.
+//
+// HBM layout (all contiguous, element = cx<T> unless noted):
+//   images  u      : local subdomains back to back, row-major [H_d][W_d]
+//   frames  Gamma  : [n_local_frames][S][S], frames ordered (local subdomain,
+//                    ascending global j) -- the reference's frames_of order
+//                    (ddplan.cpp:50-57) -- amplitudes (T) and the
+//                    back-projection scratch use the same order
+//   overlap v, Lambda, s : per local pair (ascending global p) [h][w];
+//                    Lambda and s hold side 0 (d1) then side 1 (d2)
+// plus the integer tables the kernels walk: per-frame window offsets, the
+// gather tiles with their ascending covering-frame lists, pair sides.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace pdd {
+
+// Subdomain d lives on rank floor(d * world / D).
+inline int owner_of(int d, int D, int world) { return static_cast<int>((static_cast<int64_t>(d) * world) / D); }
+
+struct Exchange {
+  int lp;        // local pair index
+  int peer;      // remote rank
+  int my_side;   // 0 or 1
+};
+
+struct Layout {
+  int D = 0, rank = 0, world = 1, S = 0;
+  std::vector<int> local_subs;  // global d, ascending
+  std::vector<int> sub_local;   // [D] -> local index or -1
+
+  int64_t nfr = 0;
+  std::vector<int64_t> fr_global;   // [nfr]
+  std::vector<int64_t> sub_fr_beg;  // [nls+1]
+  std::vector<int64_t> sub_img_off; // [nls]
+  std::vector<int32_t> sub_h, sub_w;
+  int64_t img_elems = 0;
+
+  std::vector<int64_t> fr_off;  // window corner offset into the image buffer
+  std::vector<int32_t> fr_pitch, fr_r, fr_c, fr_sub;
+
+  int tile_h = 8;
+  std::vector<int4> tiles;  // + sentinel
+  std::vector<int32_t> tile_frames;
+  std::vector<int64_t> sub_tile_beg;  // [nls+1]
+
+  std::vector<int> lpairs;          // global pair index per local pair
+  std::vector<PairGeom> pgeom;      // per local pair
+  std::vector<int32_t> sub_pbeg;    // [nls+1] CSR into psides
+  std::vector<PairSide> psides;
+  int64_t v_elems = 0, lam_elems = 0, s_elems = 0;
+  int max_pair_pix = 0;
+  std::vector<Exchange> exch;
+
+  static Layout build(const Plan& plan, int rank, int world);
+  int nls() const { return static_cast<int>(local_subs.size()); }
+  int ntiles() const { return static_cast<int>(tiles.size()) - 1; }
+};
+
+}  // namespace pdd

@@ -1,0 +1,400 @@
+// Nonblind OD²P driver: NonblindSolver (proj/src/solver.cpp) on the GPU.
+//
+// Per iteration (the paper's Steps 1-4, solver.cpp:118-205), one CUDA graph
+// node chain per rank:
+//   gate -> frame SWEEP (z/Gamma step + back-projection, RF partials of u^n)
+//        -> segsum/[all-reduce] -> rf_finalize (records RF of the previous
+//           iterate and applies the R-factor stop rule with Gamma ping-pong
+//           so a stop rolls back for free)
+//        -> pack s = u + Lambda -> [NCCL send/recv per cut pair] -> v-step
+//        -> gather (adjoint overlap-add + u-update + Lambda-update + RE)
+//        -> segsum/[all-reduce] -> re_finalize (RE stop rule, max_iters)
+// Two iterations (Gamma parities) per graph.  The R-factor of iterate n is
+// produced by the frame pass of iteration n+1 (its forward transform is the
+// reference's cached `au`), and by one trailing frame pass at the end.
+#include <chrono>
+
+#include "common.cuh"
+
+namespace pdd {
+
+void NonblindConfig::validate() const {  // solver.cpp:24-31
+  if (!(epsilon > 0.0 && epsilon < 1.0)) throw InvalidArgument("stagm: epsilon must lie in (0,1)");
+  if (eta <= 0.0 || r <= 0.0) throw InvalidArgument("NonblindConfig: eta, r must be > 0");
+  if (max_iters < 1) throw InvalidArgument("NonblindConfig: max_iters >= 1");
+  if (tol_rf <= 0.0 || tol_re <= 0.0) throw InvalidArgument("NonblindConfig: tolerances must be > 0");
+  if (threads < 0) throw InvalidArgument("NonblindConfig: threads >= 0");
+}
+
+namespace {
+
+template <typename T>
+class Nonblind final : public NonblindGpu {
+ public:
+  Nonblind(const Plan& plan, const DataSpec& data, const double* probe, const NonblindConfig& cfg,
+           const double* pin_ones, int device, Comm* comm)
+      : plan_(plan), cfg_(cfg) {
+    cfg_.validate();
+    plan.g.validate();
+    R.build(plan, data, pin_ones, device, comm, cfg.max_iters, "NonblindSolver");
+    if (R.l1 <= 0.0) throw InvalidArgument("NonblindSolver: all-zero measurements, R-factor undefined");
+    const int64_t SS = R.SS();
+    cudaStream_t s = R.st();
+    probe_ = upload(to_cx<T>(probe, SS), s);
+    probe64_ = upload(to_cx<double>(probe, SS), s);
+    const int64_t nf = R.L.nfr * SS;
+    gamma_[0].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
+    gamma_[1].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
+    bp_.alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
+    u_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.img_elems, 1));
+    v_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.v_elems, 1));
+    lam_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.lam_elems, 1));
+    s_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.s_elems, 1));
+    build_denominators();
+    layout_ = R.state_layout(plan);
+    init_state();
+  }
+
+  const StateLayout& layout() const override { return layout_; }
+
+  // solver.cpp:53-75: denom = eta * illumination_density + r per covering pair.
+  void build_denominators() {
+    cudaStream_t s = R.st();
+    DevMem dens(sizeof(double) * std::max<int64_t>(R.L.img_elems, 1));
+    GatherArgs<double> g;
+    {
+      auto gt = R.gather_args(kGatherDensity);
+      g.mode = kGatherDensity;
+      g.ntiles = gt.ntiles;
+      g.tile_h = gt.tile_h;
+      g.tiles = gt.tiles;
+      g.tile_frames = gt.tile_frames;
+      g.fr_r = gt.fr_r;
+      g.fr_c = gt.fr_c;
+      g.fr_sub = gt.fr_sub;
+      g.S = gt.S;
+      g.sub_off = gt.sub_off;
+      g.sub_h = gt.sub_h;
+      g.sub_w = gt.sub_w;
+    }
+    g.probe = probe64_.as<cx<double>>();
+    g.dens_out = dens.as<double>();
+    PDD_CUDA(launch_gather<double>(g, s));
+    denom_.alloc(sizeof(T) * std::max<int64_t>(R.L.img_elems, 1));
+    DevMem bad(sizeof(unsigned long long) * std::max(R.L.nls(), 1));
+    PDD_CUDA(cudaMemsetAsync(bad.get(), 0, bad.bytes(), s));
+    std::vector<DevMem> pins;
+    for (int ld = 0; ld < R.L.nls(); ++ld) {
+      pins.push_back(upload(R.pins[ld], s));
+      const int nps = R.L.sub_pbeg[ld + 1] - R.L.sub_pbeg[ld];
+      PDD_CUDA(launch_denom_sub<T>(dens.as<double>() + R.L.sub_img_off[ld], pins.back().as<uint8_t>(),
+                                   R.psides.template as<PairSide>() + R.L.sub_pbeg[ld], nps, R.L.sub_h[ld], R.L.sub_w[ld],
+                                   static_cast<T>(cfg_.eta), static_cast<T>(cfg_.r),
+                                   denom_.as<T>() + R.L.sub_img_off[ld], bad.as<unsigned long long>() + ld, s));
+    }
+    std::vector<unsigned long long> nbad(std::max(R.L.nls(), 1));
+    PDD_CUDA(cudaMemcpyAsync(nbad.data(), bad.get(), bad.bytes(), cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
+    for (int ld = 0; ld < R.L.nls(); ++ld)
+      if (nbad[ld])
+        throw RuntimeError("NonblindSolver: illumination density vanishes inside subdomain " +
+                           std::to_string(R.L.local_subs[ld]) +
+                           "; A_d*A_d is singular (probe/scan leave interior pixels dark)");
+  }
+
+  void init_state() override {  // solver.cpp:96-116
+    cudaStream_t s = R.st();
+    PDD_CUDA(launch_fill<T>(u_.as<cx<T>>(), R.L.img_elems, cx<T>{T(1), T(0)}, s));
+    PDD_CUDA(cudaMemsetAsync(gamma_[0].get(), 0, gamma_[0].bytes(), s));
+    PDD_CUDA(cudaMemsetAsync(lam_.get(), 0, lam_.bytes(), s));
+    R.consensus(u_.as<cx<T>>(), lam_.as<cx<T>>(), s_.as<cx<T>>(), v_.as<cx<T>>(), nullptr);
+    iter_ = 0;
+    z_valid_ = false;
+    if (z_.bytes()) {  // z^0 = A u^0
+      forward_into(z_.as<cx<T>>());
+      z_valid_ = true;
+    }
+    PDD_CUDA(cudaStreamSynchronize(s));
+  }
+
+  void forward_into(cx<T>* out, double* rf_part = nullptr) {
+    FrameArgs<T> a = R.frame_args();
+    a.probe = probe_.as<cx<T>>();
+    a.img = u_.as<cx<T>>();
+    a.frames_out = out;
+    a.rf_part = rf_part;
+    PDD_CUDA(launch_frame<T>(kFwd, R.S, a, R.st()));
+  }
+
+  // One iteration's kernels.  parity: Gamma_in = gamma_[parity].  ev (eager
+  // profiling only): events recorded around the frame and gather kernels.
+  void enqueue_iteration(int parity, bool store_z, cudaEvent_t* ev = nullptr) {
+    cudaStream_t s = R.st();
+    PDD_CUDA(launch_gate(R.ctlp(), s));
+    if (ev) PDD_CUDA(cudaEventRecord(ev[0], s));
+    FrameArgs<T> a = R.frame_args();
+    a.probe = probe_.as<cx<T>>();
+    a.img = u_.as<cx<T>>();
+    a.gamma_in = gamma_[parity].as<cx<T>>();
+    a.gamma_out = gamma_[1 - parity].as<cx<T>>();
+    a.z_out = store_z ? z_.as<cx<T>>() : nullptr;
+    a.bp_out = bp_.as<cx<T>>();
+    a.rf_part = R.rf_part.template as<double>();
+    a.stop_flag = R.skipA();
+    a.lam = static_cast<T>(cfg_.eta);
+    a.eps = static_cast<T>(cfg_.epsilon);
+    a.fast_prox = cfg_.eta <= (1.0 - cfg_.epsilon) / cfg_.epsilon;
+    PDD_CUDA(launch_frame<T>(kSweep, R.S, a, s));
+    if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
+    R.reduce_rf(true);
+    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+    R.consensus(u_.as<cx<T>>(), lam_.as<cx<T>>(), s_.as<cx<T>>(), v_.as<cx<T>>(), R.skipB());
+    GatherArgs<T> g = R.gather_args(kGatherNonblind);
+    g.bp = bp_.as<cx<T>>();
+    g.u = u_.as<cx<T>>();
+    g.denom = denom_.as<T>();
+    g.v = v_.as<cx<T>>();
+    g.lam = lam_.as<cx<T>>();
+    g.eta = static_cast<T>(cfg_.eta);
+    g.r = static_cast<T>(cfg_.r);
+    g.re_part = R.re_part.template as<double>();
+    g.stop_flag = R.skipB();
+    if (ev) PDD_CUDA(cudaEventRecord(ev[2], s));
+    PDD_CUDA(launch_gather<T>(g, s));
+    if (ev) PDD_CUDA(cudaEventRecord(ev[3], s));
+    R.reduce_re();
+    PDD_CUDA(launch_re_finalize(R.ctlp(), R.diff_sub(), R.norm_sub(), R.D, R.rec.template as<double>(), s));
+  }
+
+  // Frame pass only: records the R-factor of the current iterate.
+  void enqueue_tail(int parity) {
+    cudaStream_t s = R.st();
+    PDD_CUDA(launch_gate(R.ctlp(), s));
+    FrameArgs<T> a = R.frame_args();
+    a.probe = probe_.as<cx<T>>();
+    a.img = u_.as<cx<T>>();
+    a.rf_part = R.rf_part.template as<double>();
+    a.stop_flag = R.skipA();
+    (void)parity;
+    PDD_CUDA(launch_frame<T>(kFwd, R.S, a, s));
+    R.reduce_rf(true);
+    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+  }
+
+  void ensure_graphs() {
+    if (full_[0].ready()) return;
+    for (int p = 0; p < 2; ++p) {
+      full_[p].capture(R.st(), [&] {
+        enqueue_iteration(p, false);
+        enqueue_iteration(1 - p, false);
+      });
+      tail_[p].capture(R.st(), [&] { enqueue_tail(p); });
+    }
+  }
+
+  void ensure_z() {
+    if (!z_.bytes()) z_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.nfr * R.SS(), 1));
+  }
+
+  void step(bool store_z) override {
+    if (store_z) ensure_z();
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + 1, 2, cfg_.tol_rf, cfg_.tol_re);
+    enqueue_iteration(static_cast<int>(iter_ & 1), store_z);
+    PDD_CUDA(cudaStreamSynchronize(R.st()));
+    ++iter_;
+    z_valid_ = store_z;
+  }
+
+  // Launch iteration-pair graphs until the device reports a stop; poll every
+  // kPoll launches.  Returns per-launch milliseconds.
+  std::vector<double> drive(int max_total, bool poll) {
+    ensure_graphs();
+    constexpr int kPoll = 8;
+    cudaStream_t s = R.st();
+    std::vector<cudaEvent_t> ev;
+    std::vector<double> ms;
+    int launched = 0;
+    int parity = static_cast<int>(iter_ & 1);
+    cudaEvent_t e0;
+    PDD_CUDA(cudaEventCreate(&e0));
+    PDD_CUDA(cudaEventRecord(e0, s));
+    ev.push_back(e0);
+    while (launched < max_total) {
+      const int batch = std::min(kPoll, (max_total - launched + 1) / 2);
+      for (int b = 0; b < batch; ++b) {
+        full_[parity].launch(s);  // parity is preserved across a 2-iteration graph
+        cudaEvent_t e;
+        PDD_CUDA(cudaEventCreate(&e));
+        PDD_CUDA(cudaEventRecord(e, s));
+        ev.push_back(e);
+      }
+      launched += 2 * batch;
+      if (launched >= max_total) break;
+      if (poll && R.read_ctl().stop) break;
+    }
+    PDD_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float t = 0.f;
+      PDD_CUDA(cudaEventElapsedTime(&t, ev[i - 1], ev[i]));
+      ms.push_back(t);
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    const RunCtl c = R.read_ctl();
+    iter_ = c.iter;
+    tail_[iter_ & 1].launch(s);
+    PDD_CUDA(cudaStreamSynchronize(s));
+    return ms;
+  }
+
+  RunRecords run() override {  // solver.cpp:216-267
+    init_state();
+    R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
+    const auto ms = drive(cfg_.max_iters, true);
+    const RunCtl c = R.read_ctl();
+    RunRecords out;
+    out.iterations = c.stop ? c.stop : c.iter;
+    out.diverged_at = c.diverged;
+    std::vector<double> rec(2 * static_cast<size_t>(out.iterations));
+    if (out.iterations)
+      PDD_CUDA(cudaMemcpy(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+    for (int64_t n = 0; n < out.iterations; ++n) {
+      out.rf.push_back(rec[2 * n]);
+      out.re.push_back(rec[2 * n + 1]);
+      out.t_ms.push_back(ms.empty() ? 0.0 : ms[std::min<size_t>(n / 2, ms.size() - 1)] / 2.0);
+    }
+    iter_ = out.iterations;
+    z_valid_ = false;
+    return out;
+  }
+
+  void iterate(int n) override {
+    if (n <= 0) return;
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
+    drive(n, false);
+    z_valid_ = false;
+  }
+
+  double iterate_timed(int n) override {
+    if (n <= 0) return 0.0;
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
+    ensure_graphs();
+    cudaEvent_t e0, e1;
+    PDD_CUDA(cudaEventCreate(&e0));
+    PDD_CUDA(cudaEventCreate(&e1));
+    PDD_CUDA(cudaEventRecord(e0, R.st()));
+    drive(n, false);  // ends with the trailing R-factor pass and a stream sync
+    PDD_CUDA(cudaEventRecord(e1, R.st()));
+    PDD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PDD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    z_valid_ = false;
+    return ms;
+  }
+
+  void profile(int n, double* out) override {
+    cudaEvent_t ev[4];
+    cudaEvent_t e_start, e_end;
+    for (auto& e : ev) PDD_CUDA(cudaEventCreate(&e));
+    PDD_CUDA(cudaEventCreate(&e_start));
+    PDD_CUDA(cudaEventCreate(&e_end));
+    double fr = 0.0, ga = 0.0;
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
+    PDD_CUDA(cudaEventRecord(e_start, R.st()));
+    for (int i = 0; i < n; ++i) {
+      enqueue_iteration(static_cast<int>(iter_ & 1), false, ev);
+      PDD_CUDA(cudaEventSynchronize(ev[3]));
+      float a = 0.f, b = 0.f;
+      PDD_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+      PDD_CUDA(cudaEventElapsedTime(&b, ev[2], ev[3]));
+      fr += a;
+      ga += b;
+      ++iter_;
+    }
+    PDD_CUDA(cudaEventRecord(e_end, R.st()));
+    PDD_CUDA(cudaEventSynchronize(e_end));
+    float tot = 0.f;
+    PDD_CUDA(cudaEventElapsedTime(&tot, e_start, e_end));
+    out[0] = fr / n;
+    out[1] = ga / n;
+    out[2] = tot / n;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e_start);
+    cudaEventDestroy(e_end);
+    z_valid_ = false;
+  }
+
+  double last_rf() override {
+    const RunCtl c = R.read_ctl();
+    if (c.iter < 1) return NAN;
+    double rf = NAN;
+    PDD_CUDA(cudaMemcpy(&rf, R.rec.template as<double>() + 2 * ((c.iter - 1) % R.rec_cap), sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    return rf;
+  }
+
+  void get_state(double* u, double* z, double* gamma, double* v, double* lam, int64_t* iteration) override {
+    cudaStream_t s = R.st();
+    const int64_t nf = R.L.nfr * R.SS();
+    if (u) from_cx(download_cx<T>(u_.get(), R.L.img_elems, s), u);
+    if (gamma) from_cx(download_cx<T>(gamma_[iter_ & 1].get(), nf, s), gamma);
+    if (z) {
+      if (!z_valid_) {
+        ensure_z();
+        std::fill(z, z + 2 * nf, NAN);
+      } else {
+        from_cx(download_cx<T>(z_.get(), nf, s), z);
+      }
+    }
+    if (v) from_cx(download_cx<T>(v_.get(), R.L.v_elems, s), v);
+    if (lam) from_cx(download_cx<T>(lam_.get(), R.L.lam_elems, s), lam);
+    if (iteration) *iteration = iter_;
+  }
+
+  void set_state(const double* u, const double* z, const double* gamma, const double* v, const double* lam,
+                 int64_t iteration) override {
+    cudaStream_t s = R.st();
+    const int64_t nf = R.L.nfr * R.SS();
+    iter_ = iteration;
+    if (u) upload_cx<T>(u_.get(), u, R.L.img_elems, s);
+    if (gamma) upload_cx<T>(gamma_[iter_ & 1].get(), gamma, nf, s);
+    if (z) {
+      ensure_z();
+      upload_cx<T>(z_.get(), z, nf, s);
+      z_valid_ = true;
+    }
+    if (v) upload_cx<T>(v_.get(), v, R.L.v_elems, s);
+    if (lam) upload_cx<T>(lam_.get(), lam, R.L.lam_elems, s);
+  }
+
+  void forward_frames(double* au) override {
+    forward_into(bp_.as<cx<T>>());
+    from_cx(download_cx<T>(bp_.get(), R.L.nfr * R.SS(), R.st()), au);
+  }
+
+  void sync() override { R.stream.sync(); }
+  int64_t kernel_launches_per_iteration() const override { return 10; }
+
+ private:
+  Plan plan_;
+  NonblindConfig cfg_;
+  RankData<T> R;
+  StateLayout layout_;
+  DevMem probe_, probe64_, gamma_[2], bp_, u_, v_, lam_, s_, denom_, z_;
+  Graph full_[2], tail_[2];
+  int64_t iter_ = 0;
+  bool z_valid_ = false;
+};
+
+}  // namespace
+
+std::unique_ptr<NonblindGpu> make_nonblind(const Plan& plan, const DataSpec& data, const double* probe,
+                                           const NonblindConfig& cfg, const double* pin_ones, int dtype,
+                                           int device, Comm* comm) {
+  DeviceGuard guard(device);
+  if (dtype == 2) return std::make_unique<Nonblind<double>>(plan, data, probe, cfg, pin_ones, device, comm);
+  return std::make_unique<Nonblind<float>>(plan, data, probe, cfg, pin_ones, device, comm);
+}
+
+}  // namespace pdd

@@ -89,6 +89,11 @@ class NcclComm final : public Comm {
     a.check(a.allreduce(buf, buf, n, ncclFloat64, ncclSum, comm_, static_cast<cudaStream_t>(stream)),
             "ncclAllReduce");
   }
+  void allreduce_sum_f32(float* buf, size_t n, void* stream) override {
+    auto& a = NcclApi::get();
+    a.check(a.allreduce(buf, buf, n, ncclFloat32, ncclSum, comm_, static_cast<cudaStream_t>(stream)),
+            "ncclAllReduce");
+  }
 
  private:
   int rank_, world_;

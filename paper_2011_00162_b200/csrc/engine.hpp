@@ -56,6 +56,7 @@ struct Comm {
   virtual void send(const void* buf, size_t bytes, int peer, void* stream) = 0;
   virtual void recv(void* buf, size_t bytes, int peer, void* stream) = 0;
   virtual void allreduce_sum_f64(double* buf, size_t n, void* stream) = 0;
+  virtual void allreduce_sum_f32(float* buf, size_t n, void* stream) = 0;
 };
 
 std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int world, int device);

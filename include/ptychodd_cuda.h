@@ -199,6 +199,9 @@ PDD_API int pdd_blind_iterate(pdd_blind* h, int32_t n);
 /* w, w_copies [D_local][s][s], delta [D_local][s][s], then as nonblind */
 PDD_API int pdd_blind_get_state(pdd_blind* h, double* w, double* w_copies, double* delta, double* u, double* z,
                         double* gamma, double* v, double* lambda, int64_t* iteration);
+PDD_API int pdd_blind_set_state(pdd_blind* h, const double* w, const double* w_copies, const double* delta,
+                                const double* u, const double* z, const double* gamma, const double* v,
+                                const double* lambda, int64_t iteration);
 /* result.probe / probe_fourier (blind.cpp:440), support_mask(), the solver's own w0 */
 PDD_API int pdd_blind_get_probe(pdd_blind* h, double* probe, double* probe_fourier, double* mask, double* w0);
 PDD_API int pdd_blind_sync(pdd_blind* h);

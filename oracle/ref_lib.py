@@ -77,6 +77,7 @@ def _d(a) -> np.ndarray:
 
 
 def plan_spec(H, W, s, step, D=1, axis="auto", grid=None) -> PlanSpec:
+    """kind 0: plan_stripes(D, axis); kind 1: plan_grid(*grid)."""
     ax = {"auto": 0, "columns": 1, "rows": 2}[axis]
     if grid is not None:
         return PlanSpec(H, W, s, step, 1, grid[0] * grid[1], grid[0], grid[1], 0)

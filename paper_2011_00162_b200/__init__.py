@@ -4,10 +4,10 @@ ADMM ptychography iteration as sm_100a CUDA kernels behind a C-ABI
 """
 from ._lib import (LIB_PATH, CudaError, DivergenceError, InvalidArgument, OutOfRange, PtychoRuntimeError,
                    exported_symbols, lib)
-from .ptychodd import (ConvergenceRecord, DecompositionPlan, NonblindConfig, NonblindResult, NonblindSolver, Region,
+from .ptychodd import (BlindConfig, BlindResult, BlindSolver, BlindState, ConvergenceRecord, DecompositionPlan, NonblindConfig, NonblindResult, NonblindSolver, Region,
                        ScanGeometry, SolverState, adjoint, adjoint_probe, fft2_normalized, forward, ifft2_normalized,
                        illumination_density, intensity, make_raster_scan, merge, partition_frames, plan_grid,
                        plan_stripes, probe_density, r_factor, relative_error, restrict_overlap, scan_coverage, snr_db,
-                       stagm)
+                       stagm, disk_support_mask, estimate_support_mask)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -357,6 +357,7 @@ class Blind final : public BlindGpu {
     if (store_z) ensure_z();
     R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + 1, 2, cfg_.tol_rf, cfg_.tol_re);
     enqueue_iteration(static_cast<int>(iter_ & 1), store_z);
+    R.stream.sync();
     PDD_CUDA(cudaStreamSynchronize(R.st()));
     ++iter_;
     z_valid_ = store_z;
@@ -449,6 +450,26 @@ class Blind final : public BlindGpu {
     if (v) from_cx(download_cx<T>(v_.get(), R.L.v_elems, s), v);
     if (lam) from_cx(download_cx<T>(lam_.get(), R.L.lam_elems, s), lam);
     if (iteration) *iteration = iter_;
+  }
+
+  void set_state(const double* w, const double* wc, const double* delta, const double* u, const double* z,
+                 const double* gamma, const double* v, const double* lam, int64_t iteration) override {
+    cudaStream_t s = R.st();
+    const int64_t SS = R.SS(), nf = R.L.nfr * SS;
+    iter_ = iteration;
+    if (w) upload_cx<T>(w_.get(), w, SS, s);
+    if (wc) upload_cx<T>(wc_.get(), wc, R.L.nls() * SS, s);
+    if (delta) upload_cx<T>(delta_.get(), delta, R.L.nls() * SS, s);
+    if (u) upload_cx<T>(u_.get(), u, R.L.img_elems, s);
+    if (gamma) upload_cx<T>(gamma_[iter_ & 1].get(), gamma, nf, s);
+    if (z) {
+      ensure_z();
+      upload_cx<T>(z_.get(), z, nf, s);
+      z_valid_ = true;
+    }
+    if (v) upload_cx<T>(v_.get(), v, R.L.v_elems, s);
+    if (lam) upload_cx<T>(lam_.get(), lam, R.L.lam_elems, s);
+    refresh_wd();
   }
 
   // result.probe / probe_fourier = project_support(state.w) (blind.cpp:440)

@@ -609,6 +609,11 @@ int pdd_blind_get_state(pdd_blind* h, double* w, double* w_copies, double* delta
                         double* v, double* lambda, int64_t* iteration) {
   NB_CALL(h, h->s->get_state(w, w_copies, delta, u, z, gamma, v, lambda, iteration));
 }
+int pdd_blind_set_state(pdd_blind* h, const double* w, const double* w_copies, const double* delta, const double* u,
+                        const double* z, const double* gamma, const double* v, const double* lambda,
+                        int64_t iteration) {
+  NB_CALL(h, h->s->set_state(w, w_copies, delta, u, z, gamma, v, lambda, iteration));
+}
 int pdd_blind_get_probe(pdd_blind* h, double* probe, double* probe_fourier, double* mask, double* w0) {
   NB_CALL(h, h->s->get_probe(probe, probe_fourier, mask, w0));
 }

@@ -111,6 +111,9 @@ class BlindGpu {
   virtual void iterate(int n) = 0;
   virtual void get_state(double* w, double* w_copies, double* delta, double* u, double* z, double* gamma, double* v,
                          double* lam, int64_t* iteration) = 0;
+  virtual void set_state(const double* w, const double* w_copies, const double* delta, const double* u,
+                         const double* z, const double* gamma, const double* v, const double* lam,
+                         int64_t iteration) = 0;
   virtual void get_probe(double* probe, double* probe_fourier, double* mask, double* w0) = 0;
   virtual void sync() = 0;
   virtual int64_t kernel_launches_per_iteration() const = 0;

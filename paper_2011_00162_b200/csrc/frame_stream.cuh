@@ -1,0 +1,224 @@
+// Streamed per-frame SWEEP kernel for large frames (S = 64, 128).
+//
+// Same arithmetic as frame_kernel<..., kSweep> (the nonblind z/Gamma step of
+// solver.cpp:125-139 fused between the two transforms, then the
+// back-projection of solver.cpp:157-164), restructured around what limits a
+// 128^2 complex64 frame on one SM: the frame (128 KB) fills the shared-memory
+// transpose tile, so memory latency must be hidden *inside* the frame.
+//
+//   rows forward   : patch x probe -> 1-D FFTs of all rows -> smem (natural)
+//   column groups  : for each group of CG columns (columns are independent
+//                    once the rows are done): column FFT -> prox against
+//                    Gamma/amplitude values PREFETCHED into registers one
+//                    group ahead -> inverse column FFT -> smem
+//   rows inverse   : 1-D inverse FFTs of all rows -> x conj(probe) -> HBM
+// The Gamma/amplitude loads of group g+1 (or of the next frame's first group)
+// are issued right after group g's prox, so they land while the inverse and
+// forward column transforms run; stores are fire-and-forget.  Persistent CTAs
+// walk frames with a grid stride.  Loops over row batches and column groups
+// are not unrolled, which keeps the SASS inside the instruction cache (the
+// fully unrolled engine spent a quarter of its stall samples on
+// no_instructions, profiles/r1_frame_kernel_c4.txt).
+#pragma once
+
+#include "frame_kernel.cuh"
+
+namespace pdd {
+
+template <int S_, int NT_, int GR_, int GC_, int MINB_ = 1>
+struct StreamShape {
+  static constexpr int S = S_, NT = NT_, GR = GR_, GC = GC_, MINB = MINB_;
+  static constexpr int RR = S / GR;          // row elements per thread
+  static constexpr int RPB = NT / GR;        // rows per batch
+  static constexpr int NRB = S / RPB;        // row batches
+  static constexpr int RC = S / GC;          // column elements per thread
+  static constexpr int CG = NT / GC;         // columns per group
+  static constexpr int NG = S / CG;          // column groups
+  static constexpr int P = S + GR;           // smem pitch (bank-conflict-free with the rotation swizzle)
+  static_assert(RR >= GR && RR % GR == 0, "row split");
+  static_assert(RC >= GC && RC % GC == 0, "column split");
+  static_assert(S % RPB == 0 && S % CG == 0 && CG >= 32, "grouping");
+};
+
+template <typename T, class SH, bool FAST>
+__global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const FrameArgs<T> a) {
+  constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
+  constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
+  cx<T>* buf = tw + S;
+  double* red = reinterpret_cast<double*>(buf + S * P);
+
+  if (a.stop_flag && *a.stop_flag) return;
+  const int t = threadIdx.x;
+  for (int i = t; i < S; i += NT) tw[i] = a.tw[i];
+  __syncthreads();
+
+  const T scale = a.scale;
+  const int cx_ = t % CG, gc = t / CG;  // column-phase coordinates
+
+  // Prefetch registers: Gamma and amplitude of one column group.
+  cx<T> pg[RC];
+  T pa[RC];
+  auto prefetch = [&](int ff, int grp) {
+    if (ff >= a.nframes) return;
+    const int x = grp * CG + cx_;
+    const int64_t base = static_cast<int64_t>(ff) * S * S + x;
+#pragma unroll
+    for (int q = 0; q < RC / GC; ++q)
+#pragma unroll
+      for (int k1 = 0; k1 < GC; ++k1) {
+        const int ky = gc + GC * q + RC * k1;
+        pg[q * GC + k1] = a.gamma_in[base + static_cast<int64_t>(ky) * S];
+        pa[q * GC + k1] = a.amp[base + static_cast<int64_t>(ky) * S];
+      }
+  };
+  prefetch(blockIdx.x, 0);
+
+  for (int f = blockIdx.x; f < a.nframes; f += gridDim.x) {
+    const int64_t fbase = static_cast<int64_t>(f) * S * S;
+    // ---------------- rows, forward
+#pragma unroll 1
+    for (int rb = 0; rb < NRB; ++rb) {
+      const int y = rb * RPB + t / GR, g = t % GR;
+      cx<T> v[RR];
+      const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
+      const cx<T>* pr = a.probe + y * S + g;
+#pragma unroll
+      for (int m = 0; m < RR; ++m) v[m] = src[GR * m] * pr[GR * m];
+      dft<RR, false>(v);
+#pragma unroll
+      for (int k = 0; k < RR; ++k) {
+        const int k2 = k;
+        buf[y * P + k2 * GR + ((g + k2) & (GR - 1))] = (k == 0) ? v[k] : v[k] * tw[g * k];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RR / GR; ++q) {
+        const int k2 = g + GR * q;
+#pragma unroll
+        for (int gp = 0; gp < GR; ++gp) v[q * GR + gp] = buf[y * P + k2 * GR + ((gp + k2) & (GR - 1))];
+        dft<GR, false>(v + q * GR);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RR / GR; ++q) {
+        const int k2 = g + GR * q;
+#pragma unroll
+        for (int k1 = 0; k1 < GR; ++k1) buf[y * P + k2 + RR * k1] = v[q * GR + k1];
+      }
+    }
+    __syncthreads();
+
+    // ---------------- column groups: forward, prox, inverse
+    double rf = 0.0;
+#pragma unroll 1
+    for (int grp = 0; grp < NG; ++grp) {
+      const int x = grp * CG + cx_;
+      cx<T> w[RC];
+#pragma unroll
+      for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
+      dft<RC, false>(w);
+#pragma unroll
+      for (int k = 0; k < RC; ++k) buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * tw[gc * k];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < RC / GC; ++q) {
+        const int k2 = gc + GC * q;
+#pragma unroll
+        for (int gp = 0; gp < GC; ++gp) w[q * GC + gp] = buf[(k2 * GC + gp) * P + x];
+        dft<GC, false>(w + q * GC);
+      }
+      // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
+      T acc = T(0);
+#pragma unroll
+      for (int q = 0; q < RC / GC; ++q)
+#pragma unroll
+        for (int k1 = 0; k1 < GC; ++k1) {
+          const int e = q * GC + k1;
+          const int ky = gc + GC * q + RC * k1;
+          const int64_t idx = fbase + static_cast<int64_t>(ky) * S + x;
+          const cx<T> au = w[e] * scale;
+          acc += fabs(sqrt(norm2(au)) - pa[e]);
+          const cx<T> yv = pg[e] + au;
+          const cx<T> z = stagm_prox(yv, pa[e], a.lam, a.eps, FAST);
+          const cx<T> gn = yv - z;
+          a.gamma_out[idx] = gn;
+          if (a.z_out) a.z_out[idx] = z;
+          w[e] = z - gn;
+        }
+      rf += static_cast<double>(acc);
+      if (grp + 1 < NG) prefetch(f, grp + 1);
+      else prefetch(f + gridDim.x, 0);
+#pragma unroll
+      for (int q = 0; q < RC / GC; ++q) {
+        const int k2 = gc + GC * q;
+        dft<GC, true>(w + q * GC);
+#pragma unroll
+        for (int gp = 0; gp < GC; ++gp) buf[(k2 * GC + gp) * P + x] = w[q * GC + gp];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < RC; ++k) {
+        const cx<T> v = buf[(k * GC + gc) * P + x];
+        w[k] = (k == 0) ? v : mul_conj(v, tw[gc * k]);
+      }
+      dft<RC, true>(w);
+#pragma unroll
+      for (int m = 0; m < RC; ++m) buf[(gc + GC * m) * P + x] = w[m];
+    }
+    __syncthreads();
+
+    // ---------------- rows, inverse -> x conj(probe) -> back-projection tile
+#pragma unroll 1
+    for (int rb = 0; rb < NRB; ++rb) {
+      const int y = rb * RPB + t / GR, g = t % GR;
+      cx<T> v[RR];
+#pragma unroll
+      for (int q = 0; q < RR / GR; ++q) {
+        const int k2 = g + GR * q;
+#pragma unroll
+        for (int k1 = 0; k1 < GR; ++k1) v[q * GR + k1] = buf[y * P + k2 + RR * k1];
+        dft<GR, true>(v + q * GR);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < RR / GR; ++q) {
+        const int k2 = g + GR * q;
+#pragma unroll
+        for (int gp = 0; gp < GR; ++gp) buf[y * P + k2 * GR + ((gp + k2) & (GR - 1))] = v[q * GR + gp];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < RR; ++k) {
+        const cx<T> b = buf[y * P + k * GR + ((g + k) & (GR - 1))];
+        v[k] = (k == 0) ? b : mul_conj(b, tw[g * k]);
+      }
+      dft<RR, true>(v);
+      cx<T>* dst = a.bp_out + fbase + y * S + g;
+      const cx<T>* pr = a.probe + y * S + g;
+#pragma unroll
+      for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pr[GR * m]);
+    }
+
+    // per-frame R-factor partial (deterministic tree)
+    if (a.rf_part) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rf += __shfl_down_sync(0xffffffffu, rf, o);
+      if ((t & 31) == 0) red[t >> 5] = rf;
+    }
+    __syncthreads();  // also: rows of the next frame overwrite buf
+    if (a.rf_part && t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += red[w];
+      a.rf_part[f] = s;
+    }
+  }
+}
+
+template <typename T, class SH>
+size_t stream_smem_bytes() {
+  return sizeof(cx<T>) * (SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32);
+}
+
+}  // namespace pdd

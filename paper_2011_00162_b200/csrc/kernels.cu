@@ -16,7 +16,10 @@
 //                   (bit-identical for any GPU count at fixed D).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "frame_kernel.cuh"
+#include "frame_stream.cuh"
 #include "kernels.hpp"
 
 namespace pdd {
@@ -40,8 +43,42 @@ template <> struct FrameCfg<double, 16> { static constexpr int R = 16, FPB = 8; 
 template <> struct FrameCfg<double, 32> { static constexpr int R = 16, FPB = 2; };
 template <> struct FrameCfg<double, 64> { static constexpr int R = 16, FPB = 1; };
 
+// Streamed SWEEP kernel shapes (frame_stream.cuh) for the large frames.
+template <typename T, int S>
+struct StreamPick {
+  using type = void;
+};
+template <> struct StreamPick<float, 128> { using type = StreamShape<128, 512, 8, 8>; };
+template <> struct StreamPick<float, 64> { using type = StreamShape<64, 256, 4, 8, 2>; };
+
+template <typename T, class SH, bool FAST>
+static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
+  auto kern = sweep_stream_kernel<T, SH, FAST>;
+  const size_t smem = stream_smem_bytes<T, SH>();
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (!blocks_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, SH::NT, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
+  }
+  if (a.nframes <= 0) return cudaSuccess;
+  const int grid = std::min(a.nframes, blocks_per_sm * sms);
+  kern<<<grid, SH::NT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int S, int MODE>
 static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
+  if constexpr (MODE == kSweep && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
+    using SH = typename StreamPick<T, S>::type;
+    return a.fast_prox ? launch_stream<T, SH, true>(a, st) : launch_stream<T, SH, false>(a, st);
+  }
   using C = FrameCfg<T, S>;
   using E = Fft2<T, S, C::R>;
   constexpr int threads = E::NT * C::FPB;

@@ -710,3 +710,208 @@ class NonblindSolver(_SolverBase):
     def partitioned_frames(self):
         return partition_frames(self._data.arr if not self._data.on_device else self._data.arr.cpu().numpy(),
                                 self.plan)
+
+
+# --------------------------------------------------------------------------- blind (blind.hpp)
+@dataclass
+class BlindConfig:
+    """blind.hpp:7-22."""
+
+    epsilon: float = 0.5
+    eta: float = 0.1
+    r: float = 5.0e3
+    mu: float = 2.0e2
+    gamma: float = 1.0e-4
+    support_mask: Optional[np.ndarray] = None
+    support_energy: float = 0.995
+    max_iters: int = 1000
+    tol_rf: float = 1.0e-5
+    tol_re: float = 1.0e-3
+    stop_rule: str = "rfactor"
+    threads: int = 0
+
+    def c(self) -> L.BlindConfigC:
+        return L.BlindConfigC(self.epsilon, self.eta, self.r, self.mu, self.gamma, self.support_energy, self.tol_rf,
+                              self.tol_re, self.max_iters, 0 if self.stop_rule == "rfactor" else 1, self.threads)
+
+
+@dataclass
+class BlindState:
+    """blind.hpp:24-34."""
+
+    w: np.ndarray
+    w_copies: list
+    delta: list
+    u: list
+    z: list
+    gamma: list
+    v: list
+    lam: list
+    iteration: int = 0
+
+
+@dataclass
+class BlindResult:
+    """blind.hpp:36-46."""
+
+    probe: np.ndarray
+    probe_fourier: np.ndarray
+    support_mask: np.ndarray
+    sub_solutions: list
+    merged: np.ndarray
+    records: List[ConvergenceRecord]
+    iterations: int
+    final_rf: float
+    final_re: float
+
+
+def _freq_radius(side: int) -> np.ndarray:
+    k = np.arange(side)
+    kk = np.minimum(k, side - k).astype(float)
+    return np.sqrt(kk[:, None] ** 2 + kk[None, :] ** 2)
+
+
+def disk_support_mask(side: int, radius: float) -> np.ndarray:
+    """blind.cpp:46-52."""
+    return (_freq_radius(side) <= radius).astype(np.float64)
+
+
+def estimate_support_mask(probe_guess: np.ndarray, energy_fraction: float) -> np.ndarray:
+    """blind.cpp:54-75 (spectrum by the GPU FFT)."""
+    side = probe_guess.shape[0]
+    spec = fft2_normalized(probe_guess)
+    e = (np.abs(spec) ** 2).ravel()
+    rad = _freq_radius(side).ravel()
+    order = np.lexsort((e, rad))
+    acc = np.cumsum(e[order])
+    hit = np.nonzero(acc >= energy_fraction * float(np.cumsum(e)[-1]))[0]
+    return disk_support_mask(side, float(rad[order][hit[0]] if hit.size else rad[order][-1]))
+
+
+class BlindSolver(_SolverBase):
+    """blind.hpp:58-85 on the GPU.  ``init_state(w0)`` optionally replaces the
+    amplitude-based initial probe."""
+
+    def __init__(self, plan: DecompositionPlan, frames=None, config: Optional[BlindConfig] = None,
+                 pin_ones: Optional[np.ndarray] = None, *, amplitudes=None, dtype=None, device: int = 0,
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        self.plan, self.config = plan, config or BlindConfig()
+        g = plan.geometry
+        s = g.frame_side
+        self._data = _DataArg(frames, amplitudes)
+        self._data.validate(g)
+        m = self.config.support_mask
+        if m is not None and np.size(m) > 0 and np.shape(m) != (s, s):
+            raise InvalidArgument("BlindConfig: support mask must be frame-sized")
+        self._mask = None if (m is None or np.size(m) == 0) else f64(m)
+        if pin_ones is not None and pin_ones.shape != (g.image_height, g.image_width):
+            raise InvalidArgument("BlindSolver: pin mask shape mismatch")
+        self._pin = None if pin_ones is None else f64(pin_ones)
+        self.dtype = L.dtype_code(dtype or DEFAULT_DTYPE)
+        self.device, self.rank, self.world = device, rank, world
+        self._cfg = self.config.c()
+        h = C.c_void_p()
+        if world > 1:
+            idb = C.create_string_buffer(bytes(nccl_id), 128)
+            check(L.lib().pdd_blind_create_rank(plan.handle, ptr(self._data.arr), self._data.kind,
+                                                int(self._data.on_device), C.byref(self._cfg), ptr(self._mask),
+                                                ptr(self._pin), self.dtype, device, rank, world, idb, C.byref(h)))
+        else:
+            check(L.lib().pdd_blind_create(plan.handle, ptr(self._data.arr), self._data.kind, int(self._data.on_device),
+                                           C.byref(self._cfg), ptr(self._mask), ptr(self._pin), self.dtype, device,
+                                           C.byref(h)))
+        self._h = h
+        self._layout(L.lib().pdd_blind_layout_get, None)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and L._lib is not None:
+            L.lib().pdd_blind_destroy(h)
+            self._h = None
+
+    def _probe_info(self):
+        s = self.plan.geometry.frame_side
+        probe = np.zeros((s, s), np.complex128)
+        spec = np.zeros((s, s), np.complex128)
+        mask = np.zeros((s, s))
+        w0 = np.zeros((s, s), np.complex128)
+        check(L.lib().pdd_blind_get_probe(self._h, ptr(probe), ptr(spec), ptr(mask), ptr(w0)))
+        return probe, spec, mask, w0
+
+    def support_mask(self) -> np.ndarray:
+        return self._probe_info()[2]
+
+    def initial_probe(self) -> np.ndarray:
+        """The solver's amplitude-based w^0 (blind.cpp:123-153)."""
+        return self._probe_info()[3]
+
+    def _get_state(self) -> BlindState:
+        lay = self._lay
+        s = self.plan.geometry.frame_side
+        n = lay.n_local_sub
+        w = np.zeros((s, s), np.complex128)
+        wc = np.zeros((max(n, 1), s, s), np.complex128)
+        dl = np.zeros((max(n, 1), s, s), np.complex128)
+        u = np.zeros(lay.image_elems, np.complex128)
+        z = np.zeros(lay.frame_elems, np.complex128)
+        g = np.zeros(lay.frame_elems, np.complex128)
+        v = np.zeros(max(lay.v_elems, 1), np.complex128)
+        lam = np.zeros(max(lay.lambda_elems, 1), np.complex128)
+        it = C.c_int64()
+        check(L.lib().pdd_blind_get_state(self._h, ptr(w), ptr(wc), ptr(dl), ptr(u), ptr(z), ptr(g), ptr(v),
+                                          ptr(lam), C.byref(it)))
+        return BlindState(w, list(wc[:n]), list(dl[:n]), self._split_images(u), self._split_frames(z),
+                          self._split_frames(g), self._split_pairs(v), self._split_pairs(lam, 2), int(it.value))
+
+    def _set_state(self, st: BlindState) -> None:
+        lam = [x for pair in st.lam for x in pair]
+        check(L.lib().pdd_blind_set_state(self._h, ptr(c128(st.w)), ptr(self._cat(st.w_copies)),
+                                          ptr(self._cat(st.delta)), ptr(self._cat(st.u)), ptr(self._cat(st.z)),
+                                          ptr(self._cat(st.gamma)), ptr(self._cat(st.v)), ptr(self._cat(lam)),
+                                          C.c_int64(st.iteration)))
+
+    def init_state(self, w0: Optional[np.ndarray] = None) -> BlindState:
+        """blind.cpp:169-192."""
+        check(L.lib().pdd_blind_init_state(self._h, ptr(None if w0 is None else c128(w0))))
+        st = self._get_state()
+        return st
+
+    def step(self, state: BlindState) -> List[float]:
+        """blind.cpp:194-296 (state round-trips through host memory)."""
+        t0 = time.perf_counter()
+        self._set_state(state)
+        check(L.lib().pdd_blind_step(self._h, 1))
+        new = self._get_state()
+        for k in ("w", "w_copies", "delta", "u", "z", "gamma", "v", "lam", "iteration"):
+            setattr(state, k, getattr(new, k))
+        return [(time.perf_counter() - t0) * 1e3 for _ in self.local_subs]
+
+    def run(self, on_iteration=None, w0: Optional[np.ndarray] = None) -> BlindResult:
+        """blind.cpp:298-358 from a fresh init_state (optionally with w0)."""
+        check(L.lib().pdd_blind_init_state(self._h, ptr(None if w0 is None else c128(w0))))
+        cfg = self.config
+        n = C.c_int64()
+        div = C.c_int64()
+        rec = np.zeros((cfg.max_iters, 3))
+        rc = L.lib().pdd_blind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
+        check(rc, iteration=int(div.value))
+        records = []
+        for k in range(int(n.value)):
+            r = ConvergenceRecord(k + 1, float(rec[k, 0]), float(rec[k, 1]), None,
+                                  [float(rec[k, 2])] * len(self.local_subs), float(rec[k, 2]), float(rec[k, 2]))
+            records.append(r)
+            if on_iteration:
+                on_iteration(r)
+        st = self._get_state()
+        probe, spec, mask, _ = self._probe_info()
+        merged = merge(st.u, self.plan) if self.world == 1 else None
+        last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
+        return BlindResult(probe, spec, mask, st.u, merged, records, int(n.value), last.rf, last.re)
+
+    def iterate(self, n: int) -> None:
+        check(L.lib().pdd_blind_iterate(self._h, C.c_int32(n)))
+
+    def launches_per_iteration(self) -> int:
+        out = C.c_int64()
+        check(L.lib().pdd_blind_launches_per_iteration(self._h, C.byref(out)))
+        return int(out.value)

@@ -32,12 +32,3 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
-
-
-def rel_l2(a, b):
-    import numpy as np
-
-    a = np.asarray(a)
-    b = np.asarray(b)
-    nb = np.linalg.norm(b.ravel())
-    return float(np.linalg.norm((a - b).ravel()) / (nb if nb > 0 else 1.0))

@@ -8,7 +8,7 @@ agreement with the float64 restatement.  Tolerances: float64 compute <= 1e-10
 import numpy as np
 import pytest
 
-from conftest import rel_l2
+from tests.helpers import rel_l2
 from oracle import od2p as O
 import paper_2011_00162_b200 as P
 

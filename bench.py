@@ -286,6 +286,14 @@ def main():
     k1_bytes = 5 * p * j_local * s * s           # Gamma r/w + amplitude (compulsory)
     iter_bytes = 5 * p * J * s * s + 5 * p * sum(r.area() for r in plan.subdomains)
     peak, peak_kind = hbm_peak()
+    traffic = None
+    try:  # dram read+write per K1 launch from the committed ncu capture of this config
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            tr = json.load(fh)
+        if tr.get("config") == args.config and world == 1:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     k1_gbs = k1_bytes / (ms_frame / 1e3) / 1e9
     fft_flops = 2 * 5 * s * s * math.log2(s * s) * j_local
     launches = solver.launches_per_iteration() * args.steps + 4
@@ -296,7 +304,7 @@ def main():
                         "frames": J, "parallelism": f"subdomains over {world} GPU(s)",
                         "l2": "inputs > L2 (no flush needed)"},
                 roofline={"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
-                          "frac": k1_gbs / peak, "traffic": None, "kernel": "frame_kernel SWEEP (K1)",
+                          "frac": k1_gbs / peak, "traffic": traffic, "kernel": "frame_kernel SWEEP (K1)",
                           "kernel_ms": ms_frame, "algorithmic_bytes_per_launch": k1_bytes,
                           "peak_kind": peak_kind,
                           "fp32_tflops": fft_flops / (ms_frame / 1e3) / 1e12},

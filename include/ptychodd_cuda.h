@@ -77,6 +77,12 @@ PDD_API int pdd_plan_info_get(const pdd_plan* plan, pdd_plan_info* info);
 PDD_API int pdd_plan_arrays(const pdd_plan* plan, int64_t* positions, int32_t* assignment, int64_t* subdomains,
                     int32_t* pairs, int64_t* regions, int64_t* local_grid);
 PDD_API int pdd_plan_destroy(pdd_plan* plan);
+/* Host-only: one rank's share of a plan -- owned subdomains (d with floor(d*world/D) == rank),
+ * pairs touching them (ascending p), and the NCCL exchange schedule: one (local pair index,
+ * peer rank, my side) triple per cut pair.  Arrays sized D, n_pairs, n_pairs*3. */
+PDD_API int pdd_rank_layout(const pdd_plan* plan, int32_t rank, int32_t world, int32_t* n_local_sub,
+                            int32_t* local_subs, int32_t* n_local_pairs, int32_t* local_pairs, int32_t* n_exchange,
+                            int32_t* exchange);
 /* scan_coverage (scan.hpp:35-36): int32 [H][W] */
 PDD_API int pdd_scan_coverage(const pdd_plan* plan, int32_t* out);
 

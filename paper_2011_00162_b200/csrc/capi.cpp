@@ -10,6 +10,7 @@
 
 #include "device.hpp"
 #include "engine.hpp"
+#include "layout.hpp"
 #include "ops.hpp"
 #include "plan.hpp"
 
@@ -260,6 +261,26 @@ int pdd_plan_arrays(const pdd_plan* plan, int64_t* positions, int32_t* assignmen
 int pdd_plan_destroy(pdd_plan* plan) {
   delete plan;
   return PDD_OK;
+}
+
+int pdd_rank_layout(const pdd_plan* plan, int32_t rank, int32_t world, int32_t* n_local_sub, int32_t* local_subs,
+                    int32_t* n_local_pairs, int32_t* local_pairs, int32_t* n_exchange, int32_t* exchange) {
+  return guard([&] {
+    need(plan, "plan");
+    if (world < 1 || rank < 0 || rank >= world) throw pdd::InvalidArgument("rank_layout: bad rank/world");
+    const pdd::Layout L = pdd::Layout::build(plan->plan, rank, world);
+    if (n_local_sub) *n_local_sub = L.nls();
+    if (local_subs) std::copy(L.local_subs.begin(), L.local_subs.end(), local_subs);
+    if (n_local_pairs) *n_local_pairs = static_cast<int32_t>(L.lpairs.size());
+    if (local_pairs) std::copy(L.lpairs.begin(), L.lpairs.end(), local_pairs);
+    if (n_exchange) *n_exchange = static_cast<int32_t>(L.exch.size());
+    if (exchange)
+      for (size_t i = 0; i < L.exch.size(); ++i) {
+        exchange[3 * i] = L.exch[i].lp;
+        exchange[3 * i + 1] = L.exch[i].peer;
+        exchange[3 * i + 2] = L.exch[i].my_side;
+      }
+  });
 }
 
 int pdd_scan_coverage(const pdd_plan* plan, int32_t* out) {

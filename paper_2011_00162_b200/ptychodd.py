@@ -685,10 +685,15 @@ class NonblindSolver(_SolverBase):
             records.append(r)
             if on_iteration:
                 on_iteration(r)
-        st = self._get_state()
-        merged = merge(st.u, self.plan) if self.world == 1 else None
+        u = self._get_u()
+        merged = merge(u, self.plan) if self.world == 1 else None
         last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
-        return NonblindResult(st.u, merged, records, int(n.value), last.rf, last.re)
+        return NonblindResult(u, merged, records, int(n.value), last.rf, last.re)
+
+    def _get_u(self) -> list:
+        u = np.zeros(self._lay.image_elems, np.complex128)
+        check(L.lib().pdd_nonblind_get_state(self._h, ptr(u), None, None, None, None, None))
+        return self._split_images(u)
 
     def iterate(self, n: int) -> None:
         """Exactly n device iterations from the current state (benchmark path)."""
@@ -902,11 +907,13 @@ class BlindSolver(_SolverBase):
             records.append(r)
             if on_iteration:
                 on_iteration(r)
-        st = self._get_state()
+        u = np.zeros(self._lay.image_elems, np.complex128)
+        check(L.lib().pdd_blind_get_state(self._h, None, None, None, ptr(u), None, None, None, None, None))
+        u = self._split_images(u)
         probe, spec, mask, _ = self._probe_info()
-        merged = merge(st.u, self.plan) if self.world == 1 else None
+        merged = merge(u, self.plan) if self.world == 1 else None
         last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
-        return BlindResult(probe, spec, mask, st.u, merged, records, int(n.value), last.rf, last.re)
+        return BlindResult(probe, spec, mask, u, merged, records, int(n.value), last.rf, last.re)
 
     def iterate(self, n: int) -> None:
         check(L.lib().pdd_blind_iterate(self._h, C.c_int32(n)))

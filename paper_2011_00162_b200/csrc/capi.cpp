@@ -476,7 +476,7 @@ static int nonblind_create(const pdd_plan* plan, const void* data, int32_t kind,
     auto h = std::make_unique<pdd_nonblind>();
     h->device = device;
     DeviceScope ds(device);
-    if (world > 1) {
+    if (world > 1 || nccl_id) {  // world 1 with an id: single-rank NCCL communicator (plumbing test)
       need(nccl_id, "nccl_id");
       h->comm = pdd::make_nccl_comm(nccl_id, rank, world, device);
     }
@@ -590,7 +590,7 @@ static int blind_create(const pdd_plan* plan, const void* data, int32_t kind, in
     auto h = std::make_unique<pdd_blind>();
     h->device = device;
     DeviceScope ds(device);
-    if (world > 1) {
+    if (world > 1 || nccl_id) {
       need(nccl_id, "nccl_id");
       h->comm = pdd::make_nccl_comm(nccl_id, rank, world, device);
     }

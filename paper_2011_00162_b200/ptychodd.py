@@ -596,7 +596,7 @@ class NonblindSolver(_SolverBase):
         self.device, self.rank, self.world = device, rank, world
         self._cfg = self.config.c()
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             idb = C.create_string_buffer(bytes(nccl_id), 128)
             check(L.lib().pdd_nonblind_create_rank(plan.handle, ptr(self._data.arr), self._data.kind,
                                                    int(self._data.on_device), ptr(self.probe), C.byref(self._cfg),
@@ -816,7 +816,7 @@ class BlindSolver(_SolverBase):
         self.device, self.rank, self.world = device, rank, world
         self._cfg = self.config.c()
         h = C.c_void_p()
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             idb = C.create_string_buffer(bytes(nccl_id), 128)
             check(L.lib().pdd_blind_create_rank(plan.handle, ptr(self._data.arr), self._data.kind,
                                                 int(self._data.on_device), C.byref(self._cfg), ptr(self._mask),

@@ -21,6 +21,8 @@
 // no_instructions, profiles/r1_frame_kernel_c4.txt).
 #pragma once
 
+#include <type_traits>
+
 #include "frame_kernel.cuh"
 
 namespace pdd {
@@ -55,6 +57,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   __syncthreads();
 
   const T scale = a.scale;
+  const T inv1pl = T(1) / (T(1) + a.lam);
   const int cx_ = t % CG, gc = t / CG;  // column-phase coordinates
 
   // Prefetch registers: Gamma and amplitude of one column group.
@@ -139,9 +142,15 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
           const int ky = gc + GC * q + RC * k1;
           const int64_t idx = fbase + static_cast<int64_t>(ky) * S + x;
           const cx<T> au = w[e] * scale;
-          acc += fabs(sqrt(norm2(au)) - pa[e]);
           const cx<T> yv = pg[e] + au;
-          const cx<T> z = stagm_prox(yv, pa[e], a.lam, a.eps, FAST);
+          cx<T> z;
+          if constexpr (FAST && std::is_same_v<T, float>) {
+            acc += fabsf(abs_fast_f32(au) - pa[e]);
+            z = prox_fast_f32(yv, pa[e], a.lam, inv1pl);
+          } else {
+            acc += fabs(sqrt(norm2(au)) - pa[e]);
+            z = stagm_prox(yv, pa[e], a.lam, a.eps, FAST);
+          }
           const cx<T> gn = yv - z;
           a.gamma_out[idx] = gn;
           if (a.z_out) a.z_out[idx] = z;

@@ -170,9 +170,30 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sm) {
 
 constexpr int kMaxRowsPerThread = 4;
 
+// Streaming (evict-first) load of a complex value: back-projection tiles are
+// read exactly once.
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <typename T>
+__device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b) {
+  a.x += b.x;
+  a.y += b.y;
+  return a;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
+  constexpr int kMeta = 256;  // covering frames staged in shared memory
   __shared__ double sm[16];
+  __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta];
   if (a.stop_flag && *a.stop_flag) return;
   const int4 td = a.tiles[blockIdx.x];
   const int sub = td.x, tr0 = td.y, tc0 = td.z, fb = td.w, fe = a.tiles[blockIdx.x + 1].w;
@@ -182,6 +203,16 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   const int nrow = a.tile_h >> 3;
   const int S = a.S;
   const int64_t SS = static_cast<int64_t>(S) * S;
+  const int nf = fe - fb;
+  // frame metadata once per tile (independent loads instead of a dependent
+  // index -> corner chain inside the accumulation loop)
+  for (int k = threadIdx.x; k < nf && k < kMeta; k += blockDim.x) {
+    const int fr = a.tile_frames[fb + k];
+    s_fr[k] = fr;
+    s_r0[k] = a.fr_r[fr];
+    s_c0[k] = a.fr_c[fr];
+  }
+  __syncthreads();
 
   cx<T> acc[kMaxRowsPerThread];
   T wacc[kMaxRowsPerThread];
@@ -193,11 +224,21 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
     dacc[i] = 0.0;
   }
 
-  for (int k = fb; k < fe; ++k) {
-    const int fr = a.tile_frames[k];
-    const int cc = c - a.fr_c[fr];
+  // ascending frame order per pixel (the reference's embed_add order)
+#pragma unroll 4
+  for (int k = 0; k < nf; ++k) {
+    int fr, r0, c0;
+    if (k < kMeta) {
+      fr = s_fr[k];
+      r0 = s_r0[k];
+      c0 = s_c0[k];
+    } else {
+      fr = a.tile_frames[fb + k];
+      r0 = a.fr_r[fr];
+      c0 = a.fr_c[fr];
+    }
+    const int cc = c - c0;
     if (cc < 0 || cc >= S) continue;
-    const int r0 = a.fr_r[fr];
 #pragma unroll
     for (int i = 0; i < kMaxRowsPerThread; ++i) {
       if (i >= nrow) break;
@@ -211,7 +252,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
         acc[i] += mul_conj(a.bp[fr * SS + pix], w);
         wacc[i] += norm2(w);
       } else {
-        acc[i] += a.bp[fr * SS + pix];
+        acc[i] += __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix));
       }
     }
   }

@@ -46,6 +46,7 @@ struct FrameArgs {
   T lam = T(0), eps = T(0.5);
   int fast_prox = 1;
   T scale = T(1);                     // 1/S (unitary normalisation per transform)
+  unsigned long long* phase_cycles = nullptr;  // PDD_PHASE_TIMING builds: per-phase SM cycles
 };
 
 // ST-AGM per-pixel prox, stagm.cpp:45-73.  amp = sqrt(b).  The fast form is

@@ -78,6 +78,20 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   };
   prefetch(blockIdx.x, 0);
 
+#ifdef PDD_PHASE_TIMING
+  unsigned long long tph[4] = {0, 0, 0, 0};
+#define PDD_TICK(i)                                 \
+  do {                                              \
+    const unsigned long long now = clock64();       \
+    tph[i] += now - tlast;                          \
+    tlast = now;                                    \
+  } while (0)
+  unsigned long long tlast = clock64();
+#else
+#define PDD_TICK(i) \
+  do {              \
+  } while (0)
+#endif
   for (int f = blockIdx.x; f < a.nframes; f += gridDim.x) {
     const int64_t fbase = static_cast<int64_t>(f) * S * S;
     // ---------------- rows, forward
@@ -112,6 +126,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
     }
     __syncthreads();
+    PDD_TICK(0);
 
     // ---------------- column groups: forward, prox, inverse
     double rf = 0.0;
@@ -177,6 +192,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int m = 0; m < RC; ++m) buf[(gc + GC * m) * P + x] = w[m];
     }
     __syncthreads();
+    PDD_TICK(1);
 
     // ---------------- rows, inverse -> x conj(probe) -> back-projection tile
 #pragma unroll 1
@@ -210,6 +226,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pr[GR * m]);
     }
 
+    PDD_TICK(2);
     // per-frame R-factor partial (deterministic tree)
     if (a.rf_part) {
 #pragma unroll
@@ -222,7 +239,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int w = 0; w < NT / 32; ++w) s += red[w];
       a.rf_part[f] = s;
     }
+    PDD_TICK(3);
   }
+#ifdef PDD_PHASE_TIMING
+  if (a.phase_cycles && t == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(a.phase_cycles + i, tph[i]);
+#endif
+#undef PDD_TICK
 }
 
 template <typename T, class SH>

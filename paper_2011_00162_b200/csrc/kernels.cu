@@ -189,7 +189,7 @@ __device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b)
   return a;
 }
 
-template <typename T>
+template <typename T, int NROW>
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   constexpr int kMeta = 256;  // covering frames staged in shared memory
   __shared__ double sm[16];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int H = a.sub_h[sub], W = a.sub_w[sub];
   const int c = tc0 + tx;
-  const int nrow = a.tile_h >> 3;
+  constexpr int nrow = NROW;
   const int S = a.S;
   const int64_t SS = static_cast<int64_t>(S) * S;
   const int nf = fe - fb;
@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
     dacc[i] = 0.0;
   }
 
-  // ascending frame order per pixel (the reference's embed_add order)
+  // ascending frame order per pixel (the reference's embed_add order).
+  // Predicated loads (no per-frame branches) so the unrolled frames' loads
+  // are all in flight together; adding an exact zero for uncovered pixels
+  // leaves the sum unchanged.
 #pragma unroll 4
   for (int k = 0; k < nf; ++k) {
     int fr, r0, c0;
@@ -238,21 +241,26 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
       c0 = a.fr_c[fr];
     }
     const int cc = c - c0;
-    if (cc < 0 || cc >= S) continue;
+    const bool cv = static_cast<unsigned>(cc) < static_cast<unsigned>(S);
 #pragma unroll
-    for (int i = 0; i < kMaxRowsPerThread; ++i) {
-      if (i >= nrow) break;
+    for (int i = 0; i < nrow; ++i) {
       const int rr = tr0 + ty + 8 * i - r0;
-      if (rr < 0 || rr >= S) continue;
+      const bool v = cv && static_cast<unsigned>(rr) < static_cast<unsigned>(S);
       const int64_t pix = static_cast<int64_t>(rr) * S + cc;
       if (a.mode == kGatherDensity) {
-        dacc[i] += static_cast<double>(norm2(a.probe[pix]));
+        if (v) dacc[i] += static_cast<double>(norm2(a.probe[pix]));
       } else if (a.mode == kGatherBlind) {
-        const cx<T> w = a.probe[static_cast<int64_t>(sub) * SS + pix];
-        acc[i] += mul_conj(a.bp[fr * SS + pix], w);
+        cx<T> w{T(0), T(0)}, q{T(0), T(0)};
+        if (v) {
+          w = a.probe[static_cast<int64_t>(sub) * SS + pix];
+          q = a.bp[fr * SS + pix];
+        }
+        acc[i] += mul_conj(q, w);
         wacc[i] += norm2(w);
       } else {
-        acc[i] += __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix));
+        typename Vec2<T>::type q{T(0), T(0)};
+        if (v) q = __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix));
+        acc[i] += q;
       }
     }
   }
@@ -317,7 +325,10 @@ template <typename T>
 cudaError_t launch_gather(const GatherArgs<T>& a, cudaStream_t st) {
   if (a.ntiles <= 0) return cudaSuccess;
   if (a.tile_h < 8 || a.tile_h > 8 * kMaxRowsPerThread || a.tile_h % 8) return cudaErrorInvalidValue;
-  gather_kernel<T><<<a.ntiles, 256, 0, st>>>(a);
+  if (a.tile_h == 8) gather_kernel<T, 1><<<a.ntiles, 256, 0, st>>>(a);
+  else if (a.tile_h == 16) gather_kernel<T, 2><<<a.ntiles, 256, 0, st>>>(a);
+  else if (a.tile_h == 32) gather_kernel<T, 4><<<a.ntiles, 256, 0, st>>>(a);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

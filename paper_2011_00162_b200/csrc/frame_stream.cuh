@@ -24,6 +24,7 @@
 #include <type_traits>
 
 #include "frame_kernel.cuh"
+#include "tmem.cuh"
 
 namespace pdd {
 
@@ -42,7 +43,20 @@ struct StreamShape {
   static_assert(S % RPB == 0 && S % CG == 0 && CG >= 32, "grouping");
 };
 
-template <typename T, class SH, bool FAST>
+// TMEM columns holding one thread's probe values for all its row batches
+// (32-bit words): the probe is identical for every frame, so it is staged once
+// per persistent CTA in tensor memory instead of being re-read from L2 twice
+// per frame (64 loads/thread/frame).
+template <class SH>
+struct ProbeTmem {
+  static constexpr int PER_THREAD = SH::NRB * 2 * SH::RR;
+  static constexpr int SLOTS = (SH::NT / 32) / 4;  // warps sharing a lane quarter
+  static constexpr int RAW = PER_THREAD * SLOTS;
+  static constexpr int NCOLS = RAW <= 32 ? 32 : RAW <= 64 ? 64 : RAW <= 128 ? 128 : RAW <= 256 ? 256 : 512;
+  static_assert(RAW <= 512, "probe does not fit in TMEM");
+};
+
+template <typename T, class SH, bool FAST, bool TMEMP = false>
 __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const FrameArgs<T> a) {
   constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
@@ -54,7 +68,47 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   if (a.stop_flag && *a.stop_flag) return;
   const int t = threadIdx.x;
   for (int i = t; i < S; i += NT) tw[i] = a.tw[i];
+
+  __shared__ uint32_t tmem_slot;
+  uint32_t tmem_base = 0;
+  const int warp = t >> 5;
+  if constexpr (TMEMP) {
+    static_assert(std::is_same_v<T, float> && 2 * RR == 32, "TMEM probe path: float, 16 values per row batch");
+    if (warp == 0) tmem_alloc<ProbeTmem<SH>::NCOLS>(&tmem_slot);
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    tmem_base = tmem_slot;
+    const int col0 = (warp >> 2) * ProbeTmem<SH>::PER_THREAD;
+#pragma unroll 1
+    for (int rb = 0; rb < NRB; ++rb) {
+      const int y = rb * RPB + t / GR, g = t % GR;
+      uint32_t raw[32];
+#pragma unroll
+      for (int m = 0; m < RR; ++m) {
+        const cx<T> p = a.probe[y * S + g + GR * m];
+        raw[2 * m] = __float_as_uint(p.x);
+        raw[2 * m + 1] = __float_as_uint(p.y);
+      }
+      tmem_st32(tmem_addr(tmem_base, warp, col0 + 32 * rb), raw);
+    }
+    tmem_wait_st();
+  }
   __syncthreads();
+  // this thread's probe values for row batch rb, from TMEM or global memory
+  auto probe_row = [&](int rb, int y, int g, cx<T>* pv) {
+    if constexpr (TMEMP) {
+      uint32_t raw[32];
+      tmem_ld32(tmem_addr(tmem_base, warp, (warp >> 2) * ProbeTmem<SH>::PER_THREAD + 32 * rb), raw);
+      tmem_wait_ld();
+#pragma unroll
+      for (int m = 0; m < RR; ++m) pv[m] = cx<T>{__uint_as_float(raw[2 * m]), __uint_as_float(raw[2 * m + 1])};
+    } else {
+      const cx<T>* pr = a.probe + y * S + g;
+#pragma unroll
+      for (int m = 0; m < RR; ++m) pv[m] = pr[GR * m];
+    }
+  };
 
   const T scale = a.scale;
   const T inv1pl = T(1) / (T(1) + a.lam);
@@ -98,11 +152,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll 1
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
-      cx<T> v[RR];
+      cx<T> v[RR], pv[RR];
       const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
-      const cx<T>* pr = a.probe + y * S + g;
 #pragma unroll
-      for (int m = 0; m < RR; ++m) v[m] = src[GR * m] * pr[GR * m];
+      for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
+      probe_row(rb, y, g, pv);
+#pragma unroll
+      for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
       dft<RR, false>(v);
 #pragma unroll
       for (int k = 0; k < RR; ++k) {
@@ -198,7 +254,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll 1
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
-      cx<T> v[RR];
+      cx<T> v[RR], pv[RR];
+      probe_row(rb, y, g, pv);
 #pragma unroll
       for (int q = 0; q < RR / GR; ++q) {
         const int k2 = g + GR * q;
@@ -221,9 +278,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
       dft<RR, true>(v);
       cx<T>* dst = a.bp_out + fbase + y * S + g;
-      const cx<T>* pr = a.probe + y * S + g;
 #pragma unroll
-      for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pr[GR * m]);
+      for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pv[m]);
     }
 
     PDD_TICK(2);
@@ -246,6 +302,12 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int i = 0; i < 4; ++i) atomicAdd(a.phase_cycles + i, tph[i]);
 #endif
 #undef PDD_TICK
+  if constexpr (TMEMP) {
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    if (warp == 0) tmem_dealloc<ProbeTmem<SH>::NCOLS>(tmem_base);
+  }
 }
 
 template <typename T, class SH>

@@ -10,7 +10,7 @@
 
 using namespace pdd;
 
-template <class SH>
+template <class SH, bool USE_TMEM>
 void run(int nframes, int W) {
   constexpr int S = SH::S;
   const int64_t SS = static_cast<int64_t>(S) * S;
@@ -60,7 +60,7 @@ void run(int nframes, int W) {
   a.lam = 0.1f;
   a.eps = 0.5f;
   a.scale = 1.f / S;
-  auto kern = sweep_stream_kernel<float, SH, true>;
+  auto kern = sweep_stream_kernel<float, SH, true, USE_TMEM>;
   const size_t smem = stream_smem_bytes<float, SH>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   int bps = 0, sms = 0;
@@ -82,14 +82,16 @@ void run(int nframes, int W) {
     unsigned long long h[4];
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
     const double tot = double(h[0] + h[1] + h[2] + h[3]);
-    printf("S=%d frames=%d grid=%d (%d/SM) %.3f ms  %.2f us/frame/SM | cycles/frame: rows_fwd %.0f  cols %.0f  rows_inv %.0f  tail %.0f (total %.0f) err=%s\n",
-           S, nframes, grid, bps, ms, ms * 1e3 * grid / nframes, h[0] / double(nframes), h[1] / double(nframes),
+    printf("tmem=%d S=%d frames=%d grid=%d (%d/SM) %.3f ms  %.2f us/frame/SM | cycles/frame: rows_fwd %.0f  cols %.0f  rows_inv %.0f  tail %.0f (total %.0f) err=%s\n",
+           int(USE_TMEM), S, nframes, grid, bps, ms, ms * 1e3 * grid / nframes, h[0] / double(nframes), h[1] / double(nframes),
            h[2] / double(nframes), h[3] / double(nframes), tot / nframes, cudaGetErrorString(cudaGetLastError()));
   }
 }
 
 int main() {
-  run<StreamShape<128, 512, 8, 8>>(16384, 8192);
-  run<StreamShape<64, 256, 4, 8, 2>>(32768, 4096);
+  run<StreamShape<128, 512, 8, 8>, false>(16384, 8192);
+  run<StreamShape<128, 512, 8, 8>, true>(16384, 8192);
+  run<StreamShape<64, 256, 4, 8, 2>, false>(32768, 4096);
+  run<StreamShape<64, 256, 4, 8, 2>, true>(32768, 4096);
   return 0;
 }

@@ -83,6 +83,28 @@ def test_one_sweep_matches_oracle(dtype, tol, D, grid):
     assert abs(gs.r_factor_of(au) - osol.r_factor_of(oau)) <= tol * osol.r_factor_of(oau) * 10
 
 
+@pytest.mark.parametrize("N,s,step,grid", [(256, 64, 16, None), (512, 128, 32, None), (512, 128, 32, (2, 2)),
+                                           (384, 64, 16, (2, 3))])
+def test_streamed_sweep_large_frames_matches_oracle(N, s, step, grid):
+    """s = 64 / 128 float32 sweeps run the streamed kernel (frame_stream.cuh)."""
+    probe, f, oplan, plan = small_problem(N=N, s=s, step=step, D=2, peak=1e4, grid=grid)
+    f = fp32_intensity(f)
+    gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f32")
+    osol = O.NonblindSolver(oplan, f, probe, O.NonblindConfig())
+    st, ost = gs.init_state(), osol.init_state()
+    au, oau = [z.copy() for z in st.z], [z.copy() for z in ost.z]
+    for _ in range(2):
+        gs.step(st, au)
+        osol.step(ost, oau)
+    compare_state(st, ost, 1e-5)
+    assert abs(gs.r_factor_of(au) - osol.r_factor_of(oau)) <= 1e-5 * osol.r_factor_of(oau)
+    res = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=6, tol_rf=1e-300), dtype="f32").run()
+    _, om, orec = O.NonblindSolver(oplan, f, probe, O.NonblindConfig(max_iters=6, tol_rf=1e-300)).run()
+    assert rel_l2(res.merged, om) < 1e-4
+    assert np.max(np.abs(np.array([r.rf for r in res.records]) - [r.rf for r in orec]) /
+                  np.array([r.rf for r in orec])) < 1e-4
+
+
 def test_sweeps_f64_track_oracle_over_iterations():
     probe, f, oplan, plan = small_problem(D=2)
     gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f64")

@@ -53,7 +53,8 @@ template <> struct StreamPick<float, 64> { using type = StreamShape<64, 256, 4, 
 
 template <typename T, class SH, bool FAST>
 static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
-  auto kern = sweep_stream_kernel<T, SH, FAST, std::is_same_v<T, float>>;
+  // TMEM probe cache where it keeps occupancy (one persistent CTA per SM)
+  auto kern = sweep_stream_kernel<T, SH, FAST, std::is_same_v<T, float> && SH::MINB == 1>;
   const size_t smem = stream_smem_bytes<T, SH>();
   static int blocks_per_sm = 0;
   static int sms = 0;

@@ -438,17 +438,17 @@ class Blind final : public BlindGpu {
                  int64_t* iteration) override {
     cudaStream_t s = R.st();
     const int64_t SS = R.SS(), nf = R.L.nfr * SS;
-    if (w) from_cx(download_cx<T>(w_.get(), SS, s), w);
-    if (wc) from_cx(download_cx<T>(wc_.get(), R.L.nls() * SS, s), wc);
-    if (delta) from_cx(download_cx<T>(delta_.get(), R.L.nls() * SS, s), delta);
-    if (u) from_cx(download_cx<T>(u_.get(), R.L.img_elems, s), u);
-    if (gamma) from_cx(download_cx<T>(gamma_[iter_ & 1].get(), nf, s), gamma);
+    if (w) download_c128<T>(w_.get(), SS, w, s);
+    if (wc) download_c128<T>(wc_.get(), R.L.nls() * SS, wc, s);
+    if (delta) download_c128<T>(delta_.get(), R.L.nls() * SS, delta, s);
+    if (u) download_c128<T>(u_.get(), R.L.img_elems, u, s);
+    if (gamma) download_c128<T>(gamma_[iter_ & 1].get(), nf, gamma, s);
     if (z) {
-      if (z_valid_) from_cx(download_cx<T>(z_.get(), nf, s), z);
+      if (z_valid_) download_c128<T>(z_.get(), nf, z, s);
       else std::fill(z, z + 2 * nf, NAN);
     }
-    if (v) from_cx(download_cx<T>(v_.get(), R.L.v_elems, s), v);
-    if (lam) from_cx(download_cx<T>(lam_.get(), R.L.lam_elems, s), lam);
+    if (v) download_c128<T>(v_.get(), R.L.v_elems, v, s);
+    if (lam) download_c128<T>(lam_.get(), R.L.lam_elems, lam, s);
     if (iteration) *iteration = iter_;
   }
 

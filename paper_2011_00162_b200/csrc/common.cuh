@@ -6,7 +6,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "device.hpp"
@@ -50,6 +53,27 @@ std::vector<cx<T>> download_cx(const void* dev, int64_t n, cudaStream_t st) {
   return h;
 }
 
+// Device complex<T> -> host complex128 without a host-side conversion loop
+// (float data is widened on the device in chunks, then copied straight into
+// the caller's buffer).
+template <typename T>
+void download_c128(const void* dev, int64_t n, double* out, cudaStream_t st) {
+  if (n <= 0) return;
+  if constexpr (sizeof(T) == sizeof(double)) {
+    PDD_CUDA(cudaMemcpyAsync(out, dev, sizeof(cx<double>) * n, cudaMemcpyDeviceToHost, st));
+  } else {
+    const int64_t chunk = std::min<int64_t>(n, int64_t(32) << 20);
+    DevMem tmp(sizeof(cx<double>) * chunk);
+    for (int64_t o = 0; o < n; o += chunk) {
+      const int64_t m = std::min(chunk, n - o);
+      PDD_CUDA(launch_widen_cx(static_cast<const cx<float>*>(dev) + o, tmp.as<cx<double>>(), m, st));
+      PDD_CUDA(cudaMemcpyAsync(out + 2 * o, tmp.get(), sizeof(cx<double>) * m, cudaMemcpyDeviceToHost, st));
+      PDD_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  PDD_CUDA(cudaStreamSynchronize(st));
+}
+
 template <typename T>
 void upload_cx(void* dev, const double* src, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
@@ -57,6 +81,18 @@ void upload_cx(void* dev, const double* src, int64_t n, cudaStream_t st) {
   PDD_CUDA(cudaMemcpyAsync(dev, h.data(), sizeof(cx<T>) * n, cudaMemcpyHostToDevice, st));
   PDD_CUDA(cudaStreamSynchronize(st));
 }
+
+// PDD_TIMING=1: setup phase timings on stderr (developer aid).
+struct SetupTimer {
+  bool on = std::getenv("PDD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pdd] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 template <typename T>
 struct RankData {
@@ -89,7 +125,9 @@ struct RankData {
     device = dev;
     comm = c;
     const int rank = c ? c->rank() : 0, world = c ? c->world() : 1;
+    SetupTimer tm;
     L = Layout::build(plan, rank, world);
+    tm.mark("layout");
     S = L.S;
     D = plan.D;
     if (!frame_supported<T>(S))
@@ -123,8 +161,11 @@ struct RankData {
     rec_cap = max_iters + 2;
     rec.alloc(sizeof(double) * 2 * static_cast<size_t>(rec_cap));
 
+    tm.mark("tables");
     upload_amplitudes(plan, data);
+    tm.mark("amplitudes+l1");
     build_pins(plan, pin_ones);
+    tm.mark("pins");
   }
 
   // Measured data -> T amplitudes in local frame order, plus the R-factor

@@ -393,6 +393,18 @@ cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void widen_cx_kernel(const cx<float>* in, cx<double>* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = cx<double>{static_cast<double>(in[i].x), static_cast<double>(in[i].y)};
+}
+cudaError_t launch_widen_cx(const cx<float>* in, cx<double>* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  widen_cx_kernel<<<grid, 256, 0, st>>>(in, out, n);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 __global__ void segsum_kernel(const double* in, int stride, int comp, const int64_t* beg, const int* map,
                               double* out, const int* skip) {

@@ -87,6 +87,9 @@ cudaError_t launch_vstep(const PairGeom* pairs, int npairs, int maxpix, const cx
 template <typename T>
 cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st);
 
+// complex64 -> complex128 on the device (state downloads without host loops)
+cudaError_t launch_widen_cx(const cx<float>* in, cx<double>* out, int64_t n, cudaStream_t st);
+
 // Deterministic segmented sums: out[map[s]] = sum_{i in [beg[s], beg[s+1])} in[i*stride+comp]
 // (fixed tree; map == nullptr means identity).  Skipped when *skip != 0.
 cudaError_t launch_segsum(const double* in, int stride, int comp, const int64_t* beg, int nseg, const int* map,

@@ -50,9 +50,12 @@ class Nonblind final : public NonblindGpu {
     v_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.v_elems, 1));
     lam_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.lam_elems, 1));
     s_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.s_elems, 1));
+    SetupTimer tm;
     build_denominators();
+    tm.mark("denominators");
     layout_ = R.state_layout(plan);
     init_state();
+    tm.mark("init_state");
   }
 
   const StateLayout& layout() const override { return layout_; }
@@ -247,9 +250,12 @@ class Nonblind final : public NonblindGpu {
   }
 
   RunRecords run() override {  // solver.cpp:216-267
+    SetupTimer tm;
     init_state();
     R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
+    tm.mark("run: init");
     const auto ms = drive(cfg_.max_iters, true);
+    tm.mark("run: iterations");
     const RunCtl c = R.read_ctl();
     RunRecords out;
     out.iterations = c.stop ? c.stop : c.iter;
@@ -337,18 +343,18 @@ class Nonblind final : public NonblindGpu {
   void get_state(double* u, double* z, double* gamma, double* v, double* lam, int64_t* iteration) override {
     cudaStream_t s = R.st();
     const int64_t nf = R.L.nfr * R.SS();
-    if (u) from_cx(download_cx<T>(u_.get(), R.L.img_elems, s), u);
-    if (gamma) from_cx(download_cx<T>(gamma_[iter_ & 1].get(), nf, s), gamma);
+    if (u) download_c128<T>(u_.get(), R.L.img_elems, u, s);
+    if (gamma) download_c128<T>(gamma_[iter_ & 1].get(), nf, gamma, s);
     if (z) {
       if (!z_valid_) {
         ensure_z();
         std::fill(z, z + 2 * nf, NAN);
       } else {
-        from_cx(download_cx<T>(z_.get(), nf, s), z);
+        download_c128<T>(z_.get(), nf, z, s);
       }
     }
-    if (v) from_cx(download_cx<T>(v_.get(), R.L.v_elems, s), v);
-    if (lam) from_cx(download_cx<T>(lam_.get(), R.L.lam_elems, s), lam);
+    if (v) download_c128<T>(v_.get(), R.L.v_elems, v, s);
+    if (lam) download_c128<T>(lam_.get(), R.L.lam_elems, lam, s);
     if (iteration) *iteration = iter_;
   }
 
@@ -370,7 +376,7 @@ class Nonblind final : public NonblindGpu {
 
   void forward_frames(double* au) override {
     forward_into(bp_.as<cx<T>>());
-    from_cx(download_cx<T>(bp_.get(), R.L.nfr * R.SS(), R.st()), au);
+    download_c128<T>(bp_.get(), R.L.nfr * R.SS(), au, R.st());
   }
 
   void sync() override { R.stream.sync(); }

@@ -541,8 +541,8 @@ class _SolverBase:
 
     def _split_images(self, flat):
         out, o = [], 0
-        for h, w in self.sub_hw:
-            out.append(flat[o : o + h * w].reshape(h, w).copy())
+        for h, w in self.sub_hw:  # views into the freshly downloaded buffer
+            out.append(flat[o : o + h * w].reshape(h, w))
             o += h * w
         return out
 

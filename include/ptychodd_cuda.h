@@ -175,6 +175,8 @@ PDD_API int pdd_nonblind_set_state(pdd_nonblind* h, const double* u, const doubl
                            const double* lambda, int64_t iteration);
 /* A_d u_d of the current iterate for the local frames ([J_local][s][s] c128) */
 PDD_API int pdd_nonblind_forward(pdd_nonblind* h, double* au);
+/* merge() of the current sub-solutions on the device -> host [H][W] c128 (single-rank handles) */
+PDD_API int pdd_nonblind_merged(pdd_nonblind* h, double* out);
 PDD_API int pdd_nonblind_sync(pdd_nonblind* h);
 PDD_API int pdd_nonblind_launches_per_iteration(const pdd_nonblind* h, int64_t* n);
 PDD_API int pdd_nonblind_destroy(pdd_nonblind* h);
@@ -210,6 +212,7 @@ PDD_API int pdd_blind_set_state(pdd_blind* h, const double* w, const double* w_c
                                 const double* lambda, int64_t iteration);
 /* result.probe / probe_fourier (blind.cpp:440), support_mask(), the solver's own w0 */
 PDD_API int pdd_blind_get_probe(pdd_blind* h, double* probe, double* probe_fourier, double* mask, double* w0);
+PDD_API int pdd_blind_merged(pdd_blind* h, double* out);
 PDD_API int pdd_blind_sync(pdd_blind* h);
 PDD_API int pdd_blind_launches_per_iteration(const pdd_blind* h, int64_t* n);
 PDD_API int pdd_blind_destroy(pdd_blind* h);

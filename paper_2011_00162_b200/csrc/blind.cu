@@ -107,10 +107,8 @@ class Blind final : public BlindGpu {
 
     // rpen = r per covering pair, pinned -> -1 (blind.cpp:100-107)
     rpen_.alloc(sizeof(T) * std::max<int64_t>(R.L.img_elems, 1));
-    std::vector<DevMem> pins;
     for (int ld = 0; ld < nls; ++ld) {
-      pins.push_back(upload(R.pins[ld], s));
-      PDD_CUDA(launch_rpen_sub<T>(pins.back().template as<uint8_t>(), R.psides.template as<PairSide>() + R.L.sub_pbeg[ld],
+      PDD_CUDA(launch_rpen_sub<T>(R.pins_of(ld), R.psides.template as<PairSide>() + R.L.sub_pbeg[ld],
                                   R.L.sub_pbeg[ld + 1] - R.L.sub_pbeg[ld], R.L.sub_h[ld], R.L.sub_w[ld],
                                   static_cast<T>(cfg_.r), rpen_.as<T>() + R.L.sub_img_off[ld], s));
     }
@@ -493,6 +491,7 @@ class Blind final : public BlindGpu {
     if (w0) std::copy(w0_.begin(), w0_.end(), w0);
   }
 
+  void merged(double* out) override { R.merge_to_host(plan_, u_.as<cx<T>>(), out); }
   void sync() override { R.stream.sync(); }
   int64_t kernel_launches_per_iteration() const override { return 17; }
 

@@ -561,6 +561,7 @@ int pdd_nonblind_set_state(pdd_nonblind* h, const double* u, const double* z, co
   NB_CALL(h, h->s->set_state(u, z, gamma, v, lambda, iteration));
 }
 int pdd_nonblind_forward(pdd_nonblind* h, double* au) { NB_CALL(h, need(au, "au"); h->s->forward_frames(au)); }
+int pdd_nonblind_merged(pdd_nonblind* h, double* out) { NB_CALL(h, need(out, "out"); h->s->merged(out)); }
 int pdd_nonblind_sync(pdd_nonblind* h) { NB_CALL(h, h->s->sync()); }
 int pdd_nonblind_launches_per_iteration(const pdd_nonblind* h, int64_t* n) {
   return guard([&] {
@@ -638,6 +639,7 @@ int pdd_blind_set_state(pdd_blind* h, const double* w, const double* w_copies, c
 int pdd_blind_get_probe(pdd_blind* h, double* probe, double* probe_fourier, double* mask, double* w0) {
   NB_CALL(h, h->s->get_probe(probe, probe_fourier, mask, w0));
 }
+int pdd_blind_merged(pdd_blind* h, double* out) { NB_CALL(h, need(out, "out"); h->s->merged(out)); }
 int pdd_blind_sync(pdd_blind* h) { NB_CALL(h, h->s->sync()); }
 int pdd_blind_launches_per_iteration(const pdd_blind* h, int64_t* n) {
   return guard([&] {

@@ -106,7 +106,7 @@ struct RankData {
   DevMem sub_fr_beg, sub_tile_beg, local_map;
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
   DevMem ctl, rec;
-  std::vector<std::vector<uint8_t>> pins;  // per local subdomain
+  DevMem pin_dev;  // uint8 per local image pixel
   double l1 = 0.0;
   int D = 0;
   int rec_cap = 0;
@@ -175,26 +175,48 @@ struct RankData {
     const int64_t per = SS();
     amp.alloc(sizeof(T) * std::max<int64_t>(L.nfr * per, 1));
     const size_t esz = data.kind == kAmplitudeF32 ? 4 : 8;
-    const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (per * static_cast<int64_t>(esz)));
-    DevMem stage(esz * static_cast<size_t>(std::min(chunk, std::max<int64_t>(L.nfr, 1)) * per));
     DevMem neg(sizeof(unsigned long long));
     PDD_CUDA(cudaMemsetAsync(neg.get(), 0, neg.bytes(), s));
     const cudaMemcpyKind kind = data.device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const char* src = static_cast<const char*>(data.ptr);
-    for (int64_t f0 = 0; f0 < L.nfr; f0 += chunk) {
-      const int64_t f1 = std::min(L.nfr, f0 + chunk);
+    // Pageable host input: page-lock it for the duration of the upload (DMA at
+    // full PCIe/C2C rate instead of staged pageable copies).
+    bool registered = false;
+    const size_t total = static_cast<size_t>(plan.g.J()) * per * esz;
+    if (!data.device && total >= (size_t(64) << 20)) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeUnregistered) {
+        registered = cudaHostRegister(const_cast<char*>(src), total, cudaHostRegisterReadOnly) == cudaSuccess;
+      }
+      cudaGetLastError();
+    }
+    auto runs = [&](int64_t f0, int64_t f1, char* dst) {  // runs of consecutive global frames
       int64_t f = f0;
-      while (f < f1) {  // runs of consecutive global frames
+      while (f < f1) {
         int64_t e = f + 1;
         while (e < f1 && L.fr_global[e] == L.fr_global[e - 1] + 1) ++e;
-        PDD_CUDA(cudaMemcpyAsync(stage.as<char>() + (f - f0) * per * esz, src + L.fr_global[f] * per * esz,
-                                 (e - f) * per * esz, kind, s));
+        PDD_CUDA(cudaMemcpyAsync(dst + (f - f0) * per * esz, src + L.fr_global[f] * per * esz, (e - f) * per * esz,
+                                 kind, s));
         f = e;
       }
-      PDD_CUDA(launch_convert_amp<T>(stage.get(), data.kind, amp.as<T>() + f0 * per, (f1 - f0) * per,
-                                     neg.as<unsigned long long>(), s));
-      PDD_CUDA(cudaStreamSynchronize(s));  // stage reuse
+    };
+    const bool same = (data.kind == kAmplitudeF32 && sizeof(T) == 4) || (data.kind == kAmplitudeF64 && sizeof(T) == 8);
+    if (same) {  // straight into place, then the non-negativity check in place
+      runs(0, L.nfr, amp.as<char>());
+      PDD_CUDA(launch_convert_amp<T>(amp.get(), data.kind, amp.as<T>(), L.nfr * per, neg.as<unsigned long long>(), s));
+      PDD_CUDA(cudaStreamSynchronize(s));
+    } else {
+      const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (per * static_cast<int64_t>(esz)));
+      DevMem stage(esz * static_cast<size_t>(std::min(chunk, std::max<int64_t>(L.nfr, 1)) * per));
+      for (int64_t f0 = 0; f0 < L.nfr; f0 += chunk) {
+        const int64_t f1 = std::min(L.nfr, f0 + chunk);
+        runs(f0, f1, stage.as<char>());
+        PDD_CUDA(launch_convert_amp<T>(stage.get(), data.kind, amp.as<T>() + f0 * per, (f1 - f0) * per,
+                                       neg.as<unsigned long long>(), s));
+        PDD_CUDA(cudaStreamSynchronize(s));  // stage reuse
+      }
     }
+    if (registered) cudaHostUnregister(const_cast<char*>(src));
     unsigned long long nneg = 0;
     PDD_CUDA(cudaMemcpy(&nneg, neg.get(), sizeof(nneg), cudaMemcpyDeviceToHost));
     if (nneg) throw InvalidArgument("FrameStack: negative intensity");
@@ -213,21 +235,36 @@ struct RankData {
   }
 
   // Pixels never covered by a window, plus the caller's vacuum mask
-  // (solver.cpp:43-48, 64-69).
+  // (solver.cpp:43-48, 64-69): coverage from the gather tiles on the device.
   void build_pins(const Plan& plan, const double* pin_ones) {
-    const auto cov = scan_coverage(plan.g);
-    pins.clear();
-    for (int ld = 0; ld < L.nls(); ++ld) {
-      const Rect& sub = plan.subs[L.local_subs[ld]];
-      std::vector<uint8_t> p(static_cast<size_t>(sub.area()));
-      for (int64_t r = 0; r < sub.h(); ++r)
-        for (int64_t c = 0; c < sub.w(); ++c) {
-          const int64_t gi = (sub.r0 + r) * plan.g.W + sub.c0 + c;
-          p[r * sub.w() + c] = cov[gi] == 0 || (pin_ones && pin_ones[gi] > 0.5);
-        }
-      pins.push_back(std::move(p));
+    cudaStream_t s = st();
+    pin_dev.alloc(std::max<int64_t>(L.img_elems, 1));
+    DevMem user;
+    // Raster block plans: a subdomain's own windows tile its rectangle, so the
+    // global coverage (scan.cpp:36-44) is zero exactly where the local one is.
+    // General plans take the global coverage from the host.
+    const bool host_cov = !plan.raster_blocks;
+    if (pin_ones || host_cov) {
+      std::vector<int32_t> cov;
+      if (host_cov) cov = scan_coverage(plan.g);
+      std::vector<uint8_t> up(static_cast<size_t>(L.img_elems));
+      for (int ld = 0; ld < L.nls(); ++ld) {
+        const Rect& sub = plan.subs[L.local_subs[ld]];
+        for (int64_t r = 0; r < sub.h(); ++r)
+          for (int64_t c = 0; c < sub.w(); ++c) {
+            const int64_t gi = (sub.r0 + r) * plan.g.W + sub.c0 + c;
+            up[L.sub_img_off[ld] + r * sub.w() + c] =
+                (pin_ones && pin_ones[gi] > 0.5) || (host_cov && cov[gi] == 0);
+          }
+      }
+      user = upload(up, s);
     }
+    PDD_CUDA(launch_pins(tiles.as<int4>(), L.ntiles(), L.tile_h, tile_frames.as<int32_t>(), fr_r.as<int32_t>(),
+                         fr_c.as<int32_t>(), S, sub_off.as<int64_t>(), sub_h.as<int32_t>(), sub_w.as<int32_t>(),
+                         (pin_ones || host_cov) ? user.as<uint8_t>() : nullptr, pin_dev.as<uint8_t>(), s));
+    PDD_CUDA(cudaStreamSynchronize(s));
   }
+  const uint8_t* pins_of(int ld) const { return pin_dev.as<uint8_t>() + L.sub_img_off[ld]; }
 
   FrameArgs<T> frame_args() const {
     FrameArgs<T> a;
@@ -310,6 +347,26 @@ struct RankData {
     }
     sl.S = S;
     return sl;
+  }
+
+  // merge (ddplan.cpp:104-121) of the device sub-solutions into a host image.
+  void merge_to_host(const Plan& plan, const cx<T>* u, double* out) {
+    if (L.nls() != plan.D) throw InvalidArgument("merge: this rank does not own every subdomain");
+    cudaStream_t s = st();
+    std::vector<int64_t> rect;
+    for (const auto& r : plan.subs) {
+      rect.push_back(r.r0);
+      rect.push_back(r.r1);
+      rect.push_back(r.c0);
+      rect.push_back(r.c1);
+    }
+    DevMem drect = upload(rect, s);
+    const int64_t n = plan.g.H * plan.g.W;
+    DevMem img(sizeof(cx<double>) * n);
+    PDD_CUDA(launch_merge<T>(u, drect.as<int64_t>(), sub_off.as<int64_t>(), plan.D, plan.g.H, plan.g.W,
+                             img.as<cx<double>>(), s));
+    PDD_CUDA(cudaMemcpyAsync(out, img.get(), sizeof(cx<double>) * n, cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
   }
 
   void reset_ctl(int iter, int max_iters, int rule, double tol_rf, double tol_re) {

@@ -93,6 +93,7 @@ class NonblindGpu {
   virtual void set_state(const double* u, const double* z, const double* gamma, const double* v, const double* lam,
                          int64_t iteration) = 0;
   virtual void forward_frames(double* au) = 0;  // A_d u_d for the local frames
+  virtual void merged(double* out) = 0;         // merge() of the current sub-solutions (single rank)
   virtual void sync() = 0;
   virtual int64_t kernel_launches_per_iteration() const = 0;
 };
@@ -115,6 +116,7 @@ class BlindGpu {
                          const double* z, const double* gamma, const double* v, const double* lam,
                          int64_t iteration) = 0;
   virtual void get_probe(double* probe, double* probe_fourier, double* mask, double* w0) = 0;
+  virtual void merged(double* out) = 0;
   virtual void sync() = 0;
   virtual int64_t kernel_launches_per_iteration() const = 0;
 };

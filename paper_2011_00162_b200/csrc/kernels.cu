@@ -393,6 +393,66 @@ cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <typename T>
+__global__ void merge_kernel(const cx<T>* u, const int64_t* rect, const int64_t* off, int D, int64_t H, int64_t W,
+                             cx<double>* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < H * W;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / W, c = i % W;
+    double sx = 0.0, sy = 0.0, cnt = 0.0;
+    for (int d = 0; d < D; ++d) {
+      const int64_t* q = rect + 4 * d;
+      if (r < q[0] || r >= q[1] || c < q[2] || c >= q[3]) continue;
+      const cx<T> v = u[off[d] + (r - q[0]) * (q[3] - q[2]) + (c - q[2])];
+      sx += static_cast<double>(v.x);
+      sy += static_cast<double>(v.y);
+      cnt += 1.0;
+    }
+    out[i] = cnt > 0.0 ? cx<double>{sx / cnt, sy / cnt} : cx<double>{1.0, 0.0};
+  }
+}
+template <typename T>
+cudaError_t launch_merge(const cx<T>* u, const int64_t* sub_rect, const int64_t* sub_off, int D, int64_t H, int64_t W,
+                         cx<double>* out, cudaStream_t st) {
+  const int64_t n = H * W;
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  merge_kernel<T><<<grid, 256, 0, st>>>(u, sub_rect, sub_off, D, H, W, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_merge<float>(const cx<float>*, const int64_t*, const int64_t*, int, int64_t, int64_t,
+                                         cx<double>*, cudaStream_t);
+template cudaError_t launch_merge<double>(const cx<double>*, const int64_t*, const int64_t*, int, int64_t, int64_t,
+                                          cx<double>*, cudaStream_t);
+
+// pin = (no window covers the pixel) | user mask  -- from the gather tiles
+__global__ void pins_kernel(const int4* tiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
+                            const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
+                            const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin) {
+  const int4 td = tiles[blockIdx.x];
+  const int sub = td.x, fb = td.w, fe = tiles[blockIdx.x + 1].w;
+  const int c = td.z + (threadIdx.x & 31);
+  const int H = sub_h[sub], W = sub_w[sub];
+  for (int rr = threadIdx.x >> 5; rr < tile_h; rr += blockDim.x >> 5) {
+    const int r = td.y + rr;
+    if (r >= H || c >= W) continue;
+    bool covered = false;
+    for (int k = fb; k < fe && !covered; ++k) {
+      const int fr = tile_frames[k];
+      covered = r >= fr_r[fr] && r < fr_r[fr] + S && c >= fr_c[fr] && c < fr_c[fr] + S;
+    }
+    const int64_t i = sub_off[sub] + static_cast<int64_t>(r) * W + c;
+    pin[i] = !covered || (user_pin && user_pin[i]);
+  }
+}
+cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
+                        const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
+                        const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin, cudaStream_t st) {
+  if (ntiles <= 0) return cudaSuccess;
+  pins_kernel<<<ntiles, 256, 0, st>>>(tiles, tile_h, tile_frames, fr_r, fr_c, S, sub_off, sub_h, sub_w, user_pin, pin);
+  return cudaGetLastError();
+}
+
 __global__ void widen_cx_kernel(const cx<float>* in, cx<double>* out, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)

@@ -87,6 +87,16 @@ cudaError_t launch_vstep(const PairGeom* pairs, int npairs, int maxpix, const cx
 template <typename T>
 cudaError_t launch_fill(cx<T>* p, int64_t n, cx<T> value, cudaStream_t st);
 
+// merge (ddplan.cpp:104-121) on the device: mean over covering subdomains,
+// vacuum 1 elsewhere; subdomain rects [D][4] (r0,r1,c0,c1) with image offsets.
+template <typename T>
+cudaError_t launch_merge(const cx<T>* u, const int64_t* sub_rect, const int64_t* sub_off, int D, int64_t H, int64_t W,
+                         cx<double>* out, cudaStream_t st);
+// scan_coverage (scan.cpp:36-44) of one subdomain from its gather tiles -> pins.
+cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
+                        const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
+                        const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin, cudaStream_t st);
+
 // complex64 -> complex128 on the device (state downloads without host loops)
 cudaError_t launch_widen_cx(const cx<float>* in, cx<double>* out, int64_t n, cudaStream_t st);
 

@@ -86,11 +86,9 @@ class Nonblind final : public NonblindGpu {
     denom_.alloc(sizeof(T) * std::max<int64_t>(R.L.img_elems, 1));
     DevMem bad(sizeof(unsigned long long) * std::max(R.L.nls(), 1));
     PDD_CUDA(cudaMemsetAsync(bad.get(), 0, bad.bytes(), s));
-    std::vector<DevMem> pins;
     for (int ld = 0; ld < R.L.nls(); ++ld) {
-      pins.push_back(upload(R.pins[ld], s));
       const int nps = R.L.sub_pbeg[ld + 1] - R.L.sub_pbeg[ld];
-      PDD_CUDA(launch_denom_sub<T>(dens.as<double>() + R.L.sub_img_off[ld], pins.back().as<uint8_t>(),
+      PDD_CUDA(launch_denom_sub<T>(dens.as<double>() + R.L.sub_img_off[ld], R.pins_of(ld),
                                    R.psides.template as<PairSide>() + R.L.sub_pbeg[ld], nps, R.L.sub_h[ld], R.L.sub_w[ld],
                                    static_cast<T>(cfg_.eta), static_cast<T>(cfg_.r),
                                    denom_.as<T>() + R.L.sub_img_off[ld], bad.as<unsigned long long>() + ld, s));
@@ -379,6 +377,7 @@ class Nonblind final : public NonblindGpu {
     download_c128<T>(bp_.get(), R.L.nfr * R.SS(), au, R.st());
   }
 
+  void merged(double* out) override { R.merge_to_host(plan_, u_.as<cx<T>>(), out); }
   void sync() override { R.stream.sync(); }
   int64_t kernel_launches_per_iteration() const override { return 10; }
 

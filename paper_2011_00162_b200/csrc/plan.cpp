@@ -135,6 +135,7 @@ Plan plan_stripes(const Geometry& g, int D, int axis) {
   for (int d = 0; d < D; ++d)
     lg.emplace_back(by_cols ? g.grid_rows : b[d + 1] - b[d], by_cols ? b[d + 1] - b[d] : g.grid_cols);
   finish(plan, lg);
+  plan.raster_blocks = true;
   return plan;
 }
 
@@ -158,6 +159,7 @@ Plan plan_grid(const Geometry& g, int Dr, int Dc) {
   for (int d = 0; d < plan.D; ++d)
     lg.emplace_back(rb[d / Dc + 1] - rb[d / Dc], cb[d % Dc + 1] - cb[d % Dc]);
   finish(plan, lg);
+  plan.raster_blocks = true;
   return plan;
 }
 

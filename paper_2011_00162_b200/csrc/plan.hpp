@@ -70,6 +70,7 @@ struct Plan {
   std::vector<std::vector<int64_t>> frames_of;
   std::vector<Pair> overlaps;
   std::vector<Geometry> local;
+  bool raster_blocks = false;  // built by plan_stripes/plan_grid: every subdomain is tiled by its own windows
 
   size_t pair_index(int a, int b) const;
   Rect local_overlap(int d, size_t p) const;

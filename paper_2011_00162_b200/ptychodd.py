@@ -462,6 +462,32 @@ class SolverState:
     iteration: int = 0
 
 
+class _LazyList(list):
+    """A list filled on first access (device -> host download on demand)."""
+
+    def __init__(self, fetch):
+        super().__init__()
+        self._fetch = fetch
+        self._done = False
+
+    def _load(self):
+        if not self._done:
+            self._done = True
+            super().extend(self._fetch())
+
+    def __getitem__(self, i):
+        self._load()
+        return super().__getitem__(i)
+
+    def __iter__(self):
+        self._load()
+        return super().__iter__()
+
+    def __len__(self):
+        self._load()
+        return super().__len__()
+
+
 @dataclass
 class NonblindResult:
     """solver.hpp:53-60."""
@@ -685,8 +711,12 @@ class NonblindSolver(_SolverBase):
             records.append(r)
             if on_iteration:
                 on_iteration(r)
+        g = self.plan.geometry
+        merged = None
+        if self.world == 1:  # merged on the device (ddplan.cpp:104-121)
+            merged = np.empty((g.image_height, g.image_width), np.complex128)
+            check(L.lib().pdd_nonblind_merged(self._h, ptr(merged)))
         u = self._get_u()
-        merged = merge(u, self.plan) if self.world == 1 else None
         last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
         return NonblindResult(u, merged, records, int(n.value), last.rf, last.re)
 

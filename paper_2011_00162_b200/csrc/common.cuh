@@ -126,7 +126,7 @@ struct RankData {
     comm = c;
     const int rank = c ? c->rank() : 0, world = c ? c->world() : 1;
     SetupTimer tm;
-    L = Layout::build(plan, rank, world);
+    L = Layout::build(plan, rank, world, sizeof(T) == 4);
     tm.mark("layout");
     S = L.S;
     D = plan.D;
@@ -259,7 +259,7 @@ struct RankData {
       }
       user = upload(up, s);
     }
-    PDD_CUDA(launch_pins(tiles.as<int4>(), L.ntiles(), L.tile_h, tile_frames.as<int32_t>(), fr_r.as<int32_t>(),
+    PDD_CUDA(launch_pins(tiles.as<int4>(), L.ntiles(), L.tile_h, L.tile_w, tile_frames.as<int32_t>(), fr_r.as<int32_t>(),
                          fr_c.as<int32_t>(), S, sub_off.as<int64_t>(), sub_h.as<int32_t>(), sub_w.as<int32_t>(),
                          (pin_ones || host_cov) ? user.as<uint8_t>() : nullptr, pin_dev.as<uint8_t>(), s));
     PDD_CUDA(cudaStreamSynchronize(s));
@@ -282,6 +282,7 @@ struct RankData {
     g.mode = mode;
     g.ntiles = L.ntiles();
     g.tile_h = L.tile_h;
+    g.tile_w = L.tile_w;
     g.tiles = tiles.as<int4>();
     g.tile_frames = tile_frames.as<int32_t>();
     g.fr_r = fr_r.as<int32_t>();

@@ -95,10 +95,15 @@ __device__ __forceinline__ cx<T> stagm_prox(cx<T> y, T amp, T lam, T eps, bool f
 // float32 fast form of the prox (valid when lam <= (1-eps)/eps, see above):
 // one rsqrt replaces sqrt + two IEEE divisions; |y| and the scale factor carry
 // <= 2 ulp extra error (well inside the 1e-5 float32 parity bound).
+// rsqrt refined by one Newton step (~0.5 ulp).
+__device__ __forceinline__ float rsqrt_nr(float n2) {
+  const float r = rsqrtf(n2);
+  return r * fmaf(-0.5f * n2 * r, r, 1.5f);
+}
 __device__ __forceinline__ cx<float> prox_fast_f32(cx<float> y, float amp, float lam, float inv1pl) {
   const float n2 = norm2(y);
   if (n2 > 0.f) {
-    const float ri = rsqrtf(n2);
+    const float ri = rsqrt_nr(n2);
     const float m = (amp + lam * (n2 * ri)) * inv1pl;
     const float sc = m * ri;
     return cx<float>{y.x * sc, y.y * sc};
@@ -107,7 +112,7 @@ __device__ __forceinline__ cx<float> prox_fast_f32(cx<float> y, float amp, float
 }
 __device__ __forceinline__ float abs_fast_f32(cx<float> a) {
   const float n2 = norm2(a);
-  return n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
+  return n2 > 0.f ? n2 * rsqrt_nr(n2) : 0.f;
 }
 
 // Sum a per-thread double over the NT threads of one frame slot; result valid

@@ -190,7 +190,9 @@ __device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b)
   return a;
 }
 
-template <typename T, int NROW>
+// Gather tile: TW = 32*VEC columns x 8*NROW rows per CTA of 256 threads; lane
+// tx owns VEC adjacent columns (VEC = 2: one 16-byte load per row per frame).
+template <typename T, int NROW, int VEC>
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   constexpr int kMeta = 256;  // covering frames staged in shared memory
   __shared__ double sm[16];
@@ -200,8 +202,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   const int sub = td.x, tr0 = td.y, tc0 = td.z, fb = td.w, fe = a.tiles[blockIdx.x + 1].w;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int H = a.sub_h[sub], W = a.sub_w[sub];
-  const int c = tc0 + tx;
-  constexpr int nrow = NROW;
+  const int c = tc0 + VEC * tx;  // first of this lane's VEC columns
   const int S = a.S;
   const int64_t SS = static_cast<int64_t>(S) * S;
   const int nf = fe - fb;
@@ -215,20 +216,23 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   }
   __syncthreads();
 
-  cx<T> acc[kMaxRowsPerThread];
-  T wacc[kMaxRowsPerThread];
-  double dacc[kMaxRowsPerThread];
+  cx<T> acc[NROW][VEC];
+  T wacc[NROW][VEC];
+  double dacc[NROW][VEC];
 #pragma unroll
-  for (int i = 0; i < kMaxRowsPerThread; ++i) {
-    acc[i] = cx<T>{T(0), T(0)};
-    wacc[i] = T(0);
-    dacc[i] = 0.0;
-  }
+  for (int i = 0; i < NROW; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      acc[i][v] = cx<T>{T(0), T(0)};
+      wacc[i][v] = T(0);
+      dacc[i][v] = 0.0;
+    }
 
-  // ascending frame order per pixel (the reference's embed_add order).
-  // Predicated loads (no per-frame branches) so the unrolled frames' loads
-  // are all in flight together; adding an exact zero for uncovered pixels
-  // leaves the sum unchanged.
+  // Ascending frame order per pixel (the reference's embed_add order).
+  // Predicated loads (no per-frame branches) keep the unrolled frames' loads
+  // in flight together; adding an exact zero for uncovered pixels leaves the
+  // sum unchanged.  With VEC = 2 a frame covers both columns or neither
+  // (host guarantees even window columns, S even).
 #pragma unroll 4
   for (int k = 0; k < nf; ++k) {
     int fr, r0, c0;
@@ -244,75 +248,91 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
     const int cc = c - c0;
     const bool cv = static_cast<unsigned>(cc) < static_cast<unsigned>(S);
 #pragma unroll
-    for (int i = 0; i < nrow; ++i) {
+    for (int i = 0; i < NROW; ++i) {
       const int rr = tr0 + ty + 8 * i - r0;
-      const bool v = cv && static_cast<unsigned>(rr) < static_cast<unsigned>(S);
+      const bool ok = cv && static_cast<unsigned>(rr) < static_cast<unsigned>(S);
       const int64_t pix = static_cast<int64_t>(rr) * S + cc;
       if (a.mode == kGatherDensity) {
-        if (v) dacc[i] += static_cast<double>(norm2(a.probe[pix]));
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (ok) dacc[i][v] += static_cast<double>(norm2(a.probe[pix + v]));
       } else if (a.mode == kGatherBlind) {
-        cx<T> w{T(0), T(0)}, q{T(0), T(0)};
-        if (v) {
-          w = a.probe[static_cast<int64_t>(sub) * SS + pix];
-          q = a.bp[fr * SS + pix];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          cx<T> w{T(0), T(0)}, q{T(0), T(0)};
+          if (ok) {
+            w = a.probe[static_cast<int64_t>(sub) * SS + pix + v];
+            q = a.bp[fr * SS + pix + v];
+          }
+          acc[i][v] += mul_conj(q, w);
+          wacc[i][v] += norm2(w);
         }
-        acc[i] += mul_conj(q, w);
-        wacc[i] += norm2(w);
+      } else if constexpr (VEC == 2 && std::is_same_v<T, float>) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok) q = __ldcs(reinterpret_cast<const float4*>(a.bp + fr * SS + pix));
+        acc[i][0].x += q.x;
+        acc[i][0].y += q.y;
+        acc[i][VEC - 1].x += q.z;
+        acc[i][VEC - 1].y += q.w;
       } else {
-        typename Vec2<T>::type q{T(0), T(0)};
-        if (v) q = __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix));
-        acc[i] += q;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          typename Vec2<T>::type q{T(0), T(0)};
+          if (ok) q = __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix + v));
+          acc[i][v] += q;
+        }
       }
     }
   }
 
   double diff = 0.0, nrm = 0.0;
   const int64_t base = a.sub_off[sub];
+  const int pb = a.sub_pbeg[sub], pe = a.sub_pbeg[sub + 1];
 #pragma unroll
-  for (int i = 0; i < kMaxRowsPerThread; ++i) {
-    if (i >= nrow) break;
-    const int r = tr0 + ty + 8 * i;
-    if (r >= H || c >= W) continue;
-    const int64_t pi = base + static_cast<int64_t>(r) * W + c;
-    if (a.mode == kGatherAdjoint) {
-      a.out[pi] = acc[i];
-      continue;
+  for (int i = 0; i < NROW; ++i)
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const int r = tr0 + ty + 8 * i, cv = c + v;
+      if (r >= H || cv >= W) continue;
+      const int64_t pi = base + static_cast<int64_t>(r) * W + cv;
+      if (a.mode == kGatherAdjoint) {
+        a.out[pi] = acc[i][v];
+        continue;
+      }
+      if (a.mode == kGatherDensity) {
+        a.dens_out[pi] = dacc[i][v];
+        continue;
+      }
+      cx<T> num = acc[i][v] * a.eta;
+      for (int q = pb; q < pe; ++q) {
+        const PairSide p = a.ps[q];
+        if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
+        const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
+        num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
+      }
+      const cx<T> uo = a.u[pi];
+      cx<T> un;
+      if (a.mode == kGatherNonblind) {
+        const T d = a.denom[pi];
+        un = d < T(0) ? cx<T>{T(1), T(0)} : cx<T>{num.x / d, num.y / d};
+      } else {
+        const T rp = a.rpen[pi];
+        const T dd = a.eta * wacc[i][v] + rp + a.gamma;
+        const cx<T> nn = num + uo * a.gamma;
+        un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
+      }
+      for (int q = pb; q < pe; ++q) {
+        const PairSide p = a.ps[q];
+        if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
+        const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
+        a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
+      }
+      a.u[pi] = un;
+      const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);
+      const double dy = static_cast<double>(un.y) - static_cast<double>(uo.y);
+      diff += dx * dx + dy * dy;
+      nrm += static_cast<double>(un.x) * un.x + static_cast<double>(un.y) * un.y;
     }
-    if (a.mode == kGatherDensity) {
-      a.dens_out[pi] = dacc[i];
-      continue;
-    }
-    cx<T> num = acc[i] * a.eta;
-    const int pb = a.sub_pbeg[sub], pe = a.sub_pbeg[sub + 1];
-    for (int q = pb; q < pe; ++q) {
-      const PairSide p = a.ps[q];
-      if (r < p.r0 || r >= p.r1 || c < p.c0 || c >= p.c1) continue;
-      const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (c - p.c0);
-      num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
-    }
-    const cx<T> uo = a.u[pi];
-    cx<T> un;
-    if (a.mode == kGatherNonblind) {
-      const T d = a.denom[pi];
-      un = d < T(0) ? cx<T>{T(1), T(0)} : cx<T>{num.x / d, num.y / d};
-    } else {
-      const T rp = a.rpen[pi];
-      const T dd = a.eta * wacc[i] + rp + a.gamma;
-      const cx<T> nn = num + uo * a.gamma;
-      un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
-    }
-    for (int q = pb; q < pe; ++q) {
-      const PairSide p = a.ps[q];
-      if (r < p.r0 || r >= p.r1 || c < p.c0 || c >= p.c1) continue;
-      const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (c - p.c0);
-      a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
-    }
-    a.u[pi] = un;
-    const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);
-    const double dy = static_cast<double>(un.y) - static_cast<double>(uo.y);
-    diff += dx * dx + dy * dy;
-    nrm += static_cast<double>(un.x) * un.x + static_cast<double>(un.y) * un.y;
-  }
   if (a.re_part) {
     block_sum2(diff, nrm, sm);
     if (threadIdx.x == 0) {
@@ -325,11 +345,18 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
 template <typename T>
 cudaError_t launch_gather(const GatherArgs<T>& a, cudaStream_t st) {
   if (a.ntiles <= 0) return cudaSuccess;
-  if (a.tile_h < 8 || a.tile_h > 8 * kMaxRowsPerThread || a.tile_h % 8) return cudaErrorInvalidValue;
-  if (a.tile_h == 8) gather_kernel<T, 1><<<a.ntiles, 256, 0, st>>>(a);
-  else if (a.tile_h == 16) gather_kernel<T, 2><<<a.ntiles, 256, 0, st>>>(a);
-  else if (a.tile_h == 32) gather_kernel<T, 4><<<a.ntiles, 256, 0, st>>>(a);
-  else return cudaErrorInvalidValue;
+  if (a.tile_w == 64) {
+    if (a.tile_h != 32) return cudaErrorInvalidValue;
+    gather_kernel<T, 4, 2><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 8) {
+    gather_kernel<T, 1, 1><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 16) {
+    gather_kernel<T, 2, 1><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 32) {
+    gather_kernel<T, 4, 1><<<a.ntiles, 256, 0, st>>>(a);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
@@ -426,15 +453,14 @@ template cudaError_t launch_merge<double>(const cx<double>*, const int64_t*, con
                                           cx<double>*, cudaStream_t);
 
 // pin = (no window covers the pixel) | user mask  -- from the gather tiles
-__global__ void pins_kernel(const int4* tiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
+__global__ void pins_kernel(const int4* tiles, int tile_h, int tile_w, const int32_t* tile_frames, const int32_t* fr_r,
                             const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
                             const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin) {
   const int4 td = tiles[blockIdx.x];
   const int sub = td.x, fb = td.w, fe = tiles[blockIdx.x + 1].w;
-  const int c = td.z + (threadIdx.x & 31);
   const int H = sub_h[sub], W = sub_w[sub];
-  for (int rr = threadIdx.x >> 5; rr < tile_h; rr += blockDim.x >> 5) {
-    const int r = td.y + rr;
+  for (int e = threadIdx.x; e < tile_h * tile_w; e += blockDim.x) {
+    const int r = td.y + e / tile_w, c = td.z + e % tile_w;
     if (r >= H || c >= W) continue;
     bool covered = false;
     for (int k = fb; k < fe && !covered; ++k) {
@@ -445,11 +471,12 @@ __global__ void pins_kernel(const int4* tiles, int tile_h, const int32_t* tile_f
     pin[i] = !covered || (user_pin && user_pin[i]);
   }
 }
-cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
-                        const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
+cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, int tile_w, const int32_t* tile_frames,
+                        const int32_t* fr_r, const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
                         const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
-  pins_kernel<<<ntiles, 256, 0, st>>>(tiles, tile_h, tile_frames, fr_r, fr_c, S, sub_off, sub_h, sub_w, user_pin, pin);
+  pins_kernel<<<ntiles, 256, 0, st>>>(tiles, tile_h, tile_w, tile_frames, fr_r, fr_c, S, sub_off, sub_h, sub_w,
+                                      user_pin, pin);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,8 @@ template <typename T>
 struct GatherArgs {
   int mode = 0;
   int ntiles = 0;
-  int tile_h = 8;                       // rows per tile (multiple of 8); width is 32
+  int tile_h = 8;                       // rows per tile (multiple of 8)
+  int tile_w = 32;                      // columns per tile: 32, or 64 (float, 16-byte column pairs)
   const int4* tiles = nullptr;          // {sub, r0, c0, frame_begin}; end = tiles[i+1].w
   const int32_t* tile_frames = nullptr; // local frame ids, ascending j per tile
   const int32_t* fr_r = nullptr;        // [nframes] window corner (subdomain coords)
@@ -93,8 +94,8 @@ template <typename T>
 cudaError_t launch_merge(const cx<T>* u, const int64_t* sub_rect, const int64_t* sub_off, int D, int64_t H, int64_t W,
                          cx<double>* out, cudaStream_t st);
 // scan_coverage (scan.cpp:36-44) of one subdomain from its gather tiles -> pins.
-cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, const int32_t* tile_frames, const int32_t* fr_r,
-                        const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
+cudaError_t launch_pins(const int4* tiles, int ntiles, int tile_h, int tile_w, const int32_t* tile_frames,
+                        const int32_t* fr_r, const int32_t* fr_c, int S, const int64_t* sub_off, const int32_t* sub_h,
                         const int32_t* sub_w, const uint8_t* user_pin, uint8_t* pin, cudaStream_t st);
 
 // complex64 -> complex128 on the device (state downloads without host loops)

@@ -4,7 +4,7 @@
 
 namespace pdd {
 
-Layout Layout::build(const Plan& plan, int rank, int world) {
+Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide) {
   Layout L;
   L.D = plan.D;
   L.rank = rank;
@@ -42,7 +42,11 @@ Layout Layout::build(const Plan& plan, int rank, int world) {
 
   // gather tiles: 32 wide, tile_h high; covering frames in ascending order
   L.tile_h = L.img_elems >= (int64_t(4) << 20) ? 32 : 8;
-  const int th = L.tile_h, tw = 32;
+  // 64-wide tiles (16-byte column pairs) when every window column and S are even
+  bool even = (L.S % 2) == 0;
+  for (int32_t c : L.fr_c) even = even && (c % 2 == 0);
+  L.tile_w = (allow_wide && even && L.tile_h == 32) ? 64 : 32;
+  const int th = L.tile_h, tw = L.tile_w;
   L.sub_tile_beg.push_back(0);
   for (int ld = 0; ld < L.nls(); ++ld) {
     const int64_t H = L.sub_h[ld], W = L.sub_w[ld];

@@ -45,6 +45,7 @@ struct Layout {
   std::vector<int32_t> fr_pitch, fr_r, fr_c, fr_sub;
 
   int tile_h = 8;
+  int tile_w = 32;
   std::vector<int4> tiles;  // + sentinel
   std::vector<int32_t> tile_frames;
   std::vector<int64_t> sub_tile_beg;  // [nls+1]
@@ -57,7 +58,7 @@ struct Layout {
   int max_pair_pix = 0;
   std::vector<Exchange> exch;
 
-  static Layout build(const Plan& plan, int rank, int world);
+  static Layout build(const Plan& plan, int rank, int world, bool allow_wide = false);
   int nls() const { return static_cast<int>(local_subs.size()); }
   int ntiles() const { return static_cast<int>(tiles.size()) - 1; }
 };

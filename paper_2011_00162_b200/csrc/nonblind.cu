@@ -70,6 +70,7 @@ class Nonblind final : public NonblindGpu {
       g.mode = kGatherDensity;
       g.ntiles = gt.ntiles;
       g.tile_h = gt.tile_h;
+      g.tile_w = gt.tile_w;
       g.tiles = gt.tiles;
       g.tile_frames = gt.tile_frames;
       g.fr_r = gt.fr_r;

@@ -121,6 +121,7 @@ struct FrameOp {
     g.mode = mode;
     g.ntiles = L.ntiles();
     g.tile_h = L.tile_h;
+    g.tile_w = L.tile_w;
     g.tiles = tiles.as<int4>();
     g.tile_frames = tile_frames.as<int32_t>();
     g.fr_r = fr_r.as<int32_t>();

@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
 
   double diff = 0.0, nrm = 0.0;
   const int64_t base = a.sub_off[sub];
-  const int pb = a.sub_pbeg[sub], pe = a.sub_pbeg[sub + 1];
+  const bool update = a.mode == kGatherNonblind || a.mode == kGatherBlind;
+  const int pb = update ? a.sub_pbeg[sub] : 0, pe = update ? a.sub_pbeg[sub + 1] : 0;
 #pragma unroll
   for (int i = 0; i < NROW; ++i)
 #pragma unroll

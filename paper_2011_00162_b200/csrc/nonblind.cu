@@ -71,6 +71,8 @@ class Nonblind final : public NonblindGpu {
       g.ntiles = gt.ntiles;
       g.tile_h = gt.tile_h;
       g.tile_w = gt.tile_w;
+      g.sub_pbeg = gt.sub_pbeg;
+      g.ps = gt.ps;
       g.tiles = gt.tiles;
       g.tile_frames = gt.tile_frames;
       g.fr_r = gt.fr_r;

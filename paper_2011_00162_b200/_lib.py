@@ -11,7 +11,8 @@ import os
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libptychodd_cuda.so")
+LIB_PATH = os.environ.get("PDD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "libptychodd_cuda.so")
 
 PDD_F32, PDD_F64 = 1, 2
 DATA_INTENSITY_F64, DATA_AMPLITUDE_F32, DATA_AMPLITUDE_F64 = 0, 1, 2

@@ -62,12 +62,16 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
-  cx<T>* buf = tw + S;
+  cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
+  cx<T>* buf = twr + S;
   double* red = reinterpret_cast<double*>(buf + S * P);
 
   if (a.stop_flag && *a.stop_flag) return;
   const int t = threadIdx.x;
-  for (int i = t; i < S; i += NT) tw[i] = a.tw[i];
+  for (int i = t; i < S; i += NT) {
+    tw[i] = a.tw[i];
+    twr[i] = a.tw[(i % GR) * (i / GR)];
+  }
 
   __shared__ uint32_t tmem_slot;
   uint32_t tmem_base = 0;
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int k = 0; k < RR; ++k) {
         const int k2 = k;
-        buf[y * P + k2 * GR + ((g + k2) & (GR - 1))] = (k == 0) ? v[k] : v[k] * tw[g * k];
+        buf[y * P + k2 * GR + ((g + k2) & (GR - 1))] = (k == 0) ? v[k] : v[k] * twr[k * GR + g];
       }
       __syncwarp();
 #pragma unroll
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     PDD_TICK(0);
 
     // ---------------- column groups: forward, prox, inverse
-    double rf = 0.0;
+    T rf_acc = T(0);  // <= 2*RC terms per thread: float is ample; the tree below is double
 #pragma unroll 1
     for (int grp = 0; grp < NG; ++grp) {
       const int x = grp * CG + cx_;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
           if (a.z_out) a.z_out[idx] = z;
           w[e] = z - gn;
         }
-      rf += static_cast<double>(acc);
+      rf_acc += acc;
       if (grp + 1 < NG) prefetch(f, grp + 1);
       else prefetch(f + gridDim.x, 0);
 #pragma unroll
@@ -274,7 +278,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int k = 0; k < RR; ++k) {
         const cx<T> b = buf[y * P + k * GR + ((g + k) & (GR - 1))];
-        v[k] = (k == 0) ? b : mul_conj(b, tw[g * k]);
+        v[k] = (k == 0) ? b : mul_conj(b, twr[k * GR + g]);
       }
       dft<RR, true>(v);
       cx<T>* dst = a.bp_out + fbase + y * S + g;
@@ -284,6 +288,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
     PDD_TICK(2);
     // per-frame R-factor partial (deterministic tree)
+    double rf = static_cast<double>(rf_acc);
     if (a.rf_part) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rf += __shfl_down_sync(0xffffffffu, rf, o);
@@ -312,7 +317,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
 template <typename T, class SH>
 size_t stream_smem_bytes() {
-  return sizeof(cx<T>) * (SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32);
+  return sizeof(cx<T>) * (2 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32);
 }
 
 }  // namespace pdd

@@ -169,7 +169,6 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sm) {
   }
 }
 
-constexpr int kMaxRowsPerThread = 4;
 
 // Streaming (evict-first) load of a complex value: back-projection tiles are
 // read exactly once.
@@ -192,9 +191,12 @@ __device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b)
 
 // Gather tile: TW = 32*VEC columns x 8*NROW rows per CTA of 256 threads; lane
 // tx owns VEC adjacent columns (VEC = 2: one 16-byte load per row per frame).
-template <typename T, int NROW, int VEC>
+// MODE is a template parameter: the accumulation loop then holds no branches,
+// so the NROW x unroll predicated loads of one trip are all in flight before
+// the first add waits on one of them.
+template <typename T, int NROW, int VEC, int MODE>
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
-  constexpr int kMeta = 256;  // covering frames staged in shared memory
+  constexpr int kMeta = 256;  // covering frames staged in shared memory per chunk
   __shared__ double sm[16];
   __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta];
   if (a.stop_flag && *a.stop_flag) return;
@@ -206,15 +208,6 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   const int S = a.S;
   const int64_t SS = static_cast<int64_t>(S) * S;
   const int nf = fe - fb;
-  // frame metadata once per tile (independent loads instead of a dependent
-  // index -> corner chain inside the accumulation loop)
-  for (int k = threadIdx.x; k < nf && k < kMeta; k += blockDim.x) {
-    const int fr = a.tile_frames[fb + k];
-    s_fr[k] = fr;
-    s_r0[k] = a.fr_r[fr];
-    s_c0[k] = a.fr_c[fr];
-  }
-  __syncthreads();
 
   cx<T> acc[NROW][VEC];
   T wacc[NROW][VEC];
@@ -229,57 +222,97 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
     }
 
   // Ascending frame order per pixel (the reference's embed_add order).
-  // Predicated loads (no per-frame branches) keep the unrolled frames' loads
-  // in flight together; adding an exact zero for uncovered pixels leaves the
-  // sum unchanged.  With VEC = 2 a frame covers both columns or neither
-  // (host guarantees even window columns, S even).
-#pragma unroll 4
-  for (int k = 0; k < nf; ++k) {
-    int fr, r0, c0;
-    if (k < kMeta) {
-      fr = s_fr[k];
-      r0 = s_r0[k];
-      c0 = s_c0[k];
-    } else {
-      fr = a.tile_frames[fb + k];
-      r0 = a.fr_r[fr];
-      c0 = a.fr_c[fr];
+  // Predicated loads keep the unrolled frames' loads in flight together;
+  // adding an exact zero for uncovered pixels leaves the sum unchanged.  With
+  // VEC = 2 a frame covers both columns or neither (host guarantees even
+  // window columns, S even).
+  for (int kb = 0; kb < nf; kb += kMeta) {
+    const int nk = min(kMeta, nf - kb);
+    if (kb > 0) __syncthreads();
+    for (int k = threadIdx.x; k < nk; k += blockDim.x) {
+      const int fr = a.tile_frames[fb + kb + k];
+      s_fr[k] = fr;
+      s_r0[k] = a.fr_r[fr];
+      s_c0[k] = a.fr_c[fr];
     }
-    const int cc = c - c0;
-    const bool cv = static_cast<unsigned>(cc) < static_cast<unsigned>(S);
-#pragma unroll
-    for (int i = 0; i < NROW; ++i) {
-      const int rr = tr0 + ty + 8 * i - r0;
-      const bool ok = cv && static_cast<unsigned>(rr) < static_cast<unsigned>(S);
-      const int64_t pix = static_cast<int64_t>(rr) * S + cc;
-      if (a.mode == kGatherDensity) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          if (ok) dacc[i][v] += static_cast<double>(norm2(a.probe[pix + v]));
-      } else if (a.mode == kGatherBlind) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          cx<T> w{T(0), T(0)}, q{T(0), T(0)};
-          if (ok) {
-            w = a.probe[static_cast<int64_t>(sub) * SS + pix + v];
-            q = a.bp[fr * SS + pix + v];
-          }
-          acc[i][v] += mul_conj(q, w);
-          wacc[i][v] += norm2(w);
+    __syncthreads();
+    if constexpr (MODE == kGatherAdjoint || MODE == kGatherNonblind) {
+      // plain overlap-add: U frames x NROW rows of loads issued as one batch,
+      // then added in ascending frame order
+      using V = typename Vec2<T>::type;
+      constexpr int U = 4;
+      constexpr int NV = (VEC == 2 && std::is_same_v<T, float>) ? 1 : VEC;  // loads per row
+      using L = std::conditional_t<NV == 1 && VEC == 2, float4, V>;
+      auto load = [&](int k, int i, int v) -> L {
+        const int cc = c - s_c0[k];
+        const int rr = tr0 + ty + 8 * i - s_r0[k];
+        const bool ok = static_cast<unsigned>(cc) < static_cast<unsigned>(S) &&
+                        static_cast<unsigned>(rr) < static_cast<unsigned>(S);
+        L q{};
+        if (ok) q = __ldcs(reinterpret_cast<const L*>(a.bp + s_fr[k] * SS + static_cast<int64_t>(rr) * S + cc + v));
+        return q;
+      };
+      auto add = [&](int i, int v, const L& q) {
+        if constexpr (NV == 1 && VEC == 2) {
+          const float4 f = reinterpret_cast<const float4&>(q);
+          acc[i][0].x += f.x;
+          acc[i][0].y += f.y;
+          acc[i][VEC - 1].x += f.z;
+          acc[i][VEC - 1].y += f.w;
+        } else {
+          acc[i][v] += reinterpret_cast<const V&>(q);
         }
-      } else if constexpr (VEC == 2 && std::is_same_v<T, float>) {
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ok) q = __ldcs(reinterpret_cast<const float4*>(a.bp + fr * SS + pix));
-        acc[i][0].x += q.x;
-        acc[i][0].y += q.y;
-        acc[i][VEC - 1].x += q.z;
-        acc[i][VEC - 1].y += q.w;
-      } else {
+      };
+      int k = 0;
+#pragma unroll 1
+      for (; k + U <= nk; k += U) {
+        L q[U][NROW][NV];
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          typename Vec2<T>::type q{T(0), T(0)};
-          if (ok) q = __ldcs(reinterpret_cast<const typename Vec2<T>::type*>(a.bp + fr * SS + pix + v));
-          acc[i][v] += q;
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NROW; ++i)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) q[u][i][v] = load(k + u, i, v);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < NROW; ++i)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) add(i, v, q[u][i][v]);
+      }
+#pragma unroll 1
+      for (; k < nk; ++k)
+#pragma unroll
+        for (int i = 0; i < NROW; ++i)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) add(i, v, load(k, i, v));
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < nk; ++k) {
+        const int fr = s_fr[k], r0 = s_r0[k], c0 = s_c0[k];
+        const int cc = c - c0;
+        const bool cv = static_cast<unsigned>(cc) < static_cast<unsigned>(S);
+#pragma unroll
+        for (int i = 0; i < NROW; ++i) {
+          const int rr = tr0 + ty + 8 * i - r0;
+          const bool ok = cv && static_cast<unsigned>(rr) < static_cast<unsigned>(S);
+          const int64_t pix = static_cast<int64_t>(rr) * S + cc;
+          if constexpr (MODE == kGatherDensity) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v)
+              if (ok) dacc[i][v] += static_cast<double>(norm2(a.probe[pix + v]));
+          } else {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              cx<T> w{T(0), T(0)}, q{T(0), T(0)};
+              if (ok) {
+                w = a.probe[static_cast<int64_t>(sub) * SS + pix + v];
+                q = a.bp[fr * SS + pix + v];
+              }
+              acc[i][v] += mul_conj(q, w);
+              wacc[i][v] += norm2(w);
+            }
+          }
         }
       }
     }
@@ -287,8 +320,12 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
 
   double diff = 0.0, nrm = 0.0;
   const int64_t base = a.sub_off[sub];
-  const bool update = a.mode == kGatherNonblind || a.mode == kGatherBlind;
-  const int pb = update ? a.sub_pbeg[sub] : 0, pe = update ? a.sub_pbeg[sub + 1] : 0;
+  constexpr bool update = MODE == kGatherNonblind || MODE == kGatherBlind;
+  int pb = 0, pe = 0;
+  if constexpr (update) {
+    pb = a.sub_pbeg[sub];
+    pe = a.sub_pbeg[sub + 1];
+  }
 #pragma unroll
   for (int i = 0; i < NROW; ++i)
 #pragma unroll
@@ -296,69 +333,80 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
       const int r = tr0 + ty + 8 * i, cv = c + v;
       if (r >= H || cv >= W) continue;
       const int64_t pi = base + static_cast<int64_t>(r) * W + cv;
-      if (a.mode == kGatherAdjoint) {
+      if constexpr (MODE == kGatherAdjoint) {
         a.out[pi] = acc[i][v];
-        continue;
-      }
-      if (a.mode == kGatherDensity) {
+      } else if constexpr (MODE == kGatherDensity) {
         a.dens_out[pi] = dacc[i][v];
-        continue;
-      }
-      cx<T> num = acc[i][v] * a.eta;
-      for (int q = pb; q < pe; ++q) {
-        const PairSide p = a.ps[q];
-        if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
-        const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
-        num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
-      }
-      const cx<T> uo = a.u[pi];
-      cx<T> un;
-      if (a.mode == kGatherNonblind) {
-        const T d = a.denom[pi];
-        un = d < T(0) ? cx<T>{T(1), T(0)} : cx<T>{num.x / d, num.y / d};
       } else {
-        const T rp = a.rpen[pi];
-        const T dd = a.eta * wacc[i][v] + rp + a.gamma;
-        const cx<T> nn = num + uo * a.gamma;
-        un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
+        cx<T> num = acc[i][v] * a.eta;
+        for (int q = pb; q < pe; ++q) {
+          const PairSide p = a.ps[q];
+          if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
+          const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
+          num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
+        }
+        const cx<T> uo = a.u[pi];
+        cx<T> un;
+        if constexpr (MODE == kGatherNonblind) {
+          const T d = a.denom[pi];
+          un = d < T(0) ? cx<T>{T(1), T(0)} : cx<T>{num.x / d, num.y / d};
+        } else {
+          const T rp = a.rpen[pi];
+          const T dd = a.eta * wacc[i][v] + rp + a.gamma;
+          const cx<T> nn = num + uo * a.gamma;
+          un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
+        }
+        for (int q = pb; q < pe; ++q) {
+          const PairSide p = a.ps[q];
+          if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
+          const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
+          a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
+        }
+        a.u[pi] = un;
+        const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);
+        const double dy = static_cast<double>(un.y) - static_cast<double>(uo.y);
+        diff += dx * dx + dy * dy;
+        nrm += static_cast<double>(un.x) * un.x + static_cast<double>(un.y) * un.y;
       }
-      for (int q = pb; q < pe; ++q) {
-        const PairSide p = a.ps[q];
-        if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
-        const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
-        a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
-      }
-      a.u[pi] = un;
-      const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);
-      const double dy = static_cast<double>(un.y) - static_cast<double>(uo.y);
-      diff += dx * dx + dy * dy;
-      nrm += static_cast<double>(un.x) * un.x + static_cast<double>(un.y) * un.y;
     }
-  if (a.re_part) {
-    block_sum2(diff, nrm, sm);
-    if (threadIdx.x == 0) {
-      a.re_part[2 * blockIdx.x] = diff;
-      a.re_part[2 * blockIdx.x + 1] = nrm;
+  if constexpr (update) {
+    if (a.re_part) {
+      block_sum2(diff, nrm, sm);
+      if (threadIdx.x == 0) {
+        a.re_part[2 * blockIdx.x] = diff;
+        a.re_part[2 * blockIdx.x + 1] = nrm;
+      }
     }
   }
+}
+
+template <typename T, int MODE>
+static cudaError_t launch_gather_mode(const GatherArgs<T>& a, cudaStream_t st) {
+  if (a.tile_w == 64) {
+    if (a.tile_h != 32) return cudaErrorInvalidValue;
+    gather_kernel<T, 4, 2, MODE><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 8) {
+    gather_kernel<T, 1, 1, MODE><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 16) {
+    gather_kernel<T, 2, 1, MODE><<<a.ntiles, 256, 0, st>>>(a);
+  } else if (a.tile_h == 32) {
+    gather_kernel<T, 4, 1, MODE><<<a.ntiles, 256, 0, st>>>(a);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_gather(const GatherArgs<T>& a, cudaStream_t st) {
   if (a.ntiles <= 0) return cudaSuccess;
-  if (a.tile_w == 64) {
-    if (a.tile_h != 32) return cudaErrorInvalidValue;
-    gather_kernel<T, 4, 2><<<a.ntiles, 256, 0, st>>>(a);
-  } else if (a.tile_h == 8) {
-    gather_kernel<T, 1, 1><<<a.ntiles, 256, 0, st>>>(a);
-  } else if (a.tile_h == 16) {
-    gather_kernel<T, 2, 1><<<a.ntiles, 256, 0, st>>>(a);
-  } else if (a.tile_h == 32) {
-    gather_kernel<T, 4, 1><<<a.ntiles, 256, 0, st>>>(a);
-  } else {
-    return cudaErrorInvalidValue;
+  switch (a.mode) {
+    case kGatherAdjoint: return launch_gather_mode<T, kGatherAdjoint>(a, st);
+    case kGatherNonblind: return launch_gather_mode<T, kGatherNonblind>(a, st);
+    case kGatherBlind: return launch_gather_mode<T, kGatherBlind>(a, st);
+    case kGatherDensity: return launch_gather_mode<T, kGatherDensity>(a, st);
+    default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

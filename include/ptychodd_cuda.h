@@ -175,6 +175,13 @@ PDD_API int pdd_nonblind_set_state(pdd_nonblind* h, const double* u, const doubl
                            const double* lambda, int64_t iteration);
 /* A_d u_d of the current iterate for the local frames ([J_local][s][s] c128) */
 PDD_API int pdd_nonblind_forward(pdd_nonblind* h, double* au);
+/* augmented_lagrangian (metrics.hpp:16-19, metrics.cpp:73-101) of the handle's current state
+ * (u, z, Gamma, v, Lambda) with au = A u recomputed on the device.  Needs a stored z (init_state,
+ * set_state with z, or step with store_z); otherwise PDD_INVALID_ARGUMENT.  Collective over ranks. */
+PDD_API int pdd_nonblind_lagrangian(pdd_nonblind* h, double* out);
+/* ConvergenceRecord::lagrangian history of the last run() with record_lagrangian (solver.cpp:258-260):
+ * copies min(cap, n) values, *n = recorded count (0 when record_lagrangian was off). */
+PDD_API int pdd_nonblind_lagrangian_history(pdd_nonblind* h, double* out, int64_t cap, int64_t* n);
 /* merge() of the current sub-solutions on the device -> host [H][W] c128 (single-rank handles) */
 PDD_API int pdd_nonblind_merged(pdd_nonblind* h, double* out);
 PDD_API int pdd_nonblind_sync(pdd_nonblind* h);

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -561,6 +562,13 @@ int pdd_nonblind_set_state(pdd_nonblind* h, const double* u, const double* z, co
   NB_CALL(h, h->s->set_state(u, z, gamma, v, lambda, iteration));
 }
 int pdd_nonblind_forward(pdd_nonblind* h, double* au) { NB_CALL(h, need(au, "au"); h->s->forward_frames(au)); }
+int pdd_nonblind_lagrangian(pdd_nonblind* h, double* out) {
+  NB_CALL(h, need(out, "out"); *out = h->s->lagrangian());
+}
+int pdd_nonblind_lagrangian_history(pdd_nonblind* h, double* out, int64_t cap, int64_t* n) {
+  NB_CALL(h, need(n, "n"); const auto v = h->s->lagrangian_history(); *n = static_cast<int64_t>(v.size());
+          if (out) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, *n), out));
+}
 int pdd_nonblind_merged(pdd_nonblind* h, double* out) { NB_CALL(h, need(out, "out"); h->s->merged(out)); }
 int pdd_nonblind_sync(pdd_nonblind* h) { NB_CALL(h, h->s->sync()); }
 int pdd_nonblind_launches_per_iteration(const pdd_nonblind* h, int64_t* n) {

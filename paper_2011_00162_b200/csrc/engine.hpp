@@ -42,6 +42,7 @@ struct RunRecords {
   int64_t iterations = 0;
   int64_t diverged_at = 0;  // > 0: non-finite RF/RE at this iteration
   std::vector<double> rf, re, t_ms;
+  std::vector<double> lag;  // augmented Lagrangian per iteration (record_lagrangian runs)
 };
 
 // Peer transport for the overlap exchange and the scalar all-reduce
@@ -93,6 +94,11 @@ class NonblindGpu {
   virtual void set_state(const double* u, const double* z, const double* gamma, const double* v, const double* lam,
                          int64_t iteration) = 0;
   virtual void forward_frames(double* au) = 0;  // A_d u_d for the local frames
+  // Augmented Lagrangian (metrics.cpp:73-101) of the current state; needs z
+  // (init_state, set_state with z, or step with store_z).
+  virtual double lagrangian() = 0;
+  // Per-iteration values recorded by the last run() with record_lagrangian.
+  virtual std::vector<double> lagrangian_history() const = 0;
   virtual void merged(double* out) = 0;         // merge() of the current sub-solutions (single rank)
   virtual void sync() = 0;
   virtual int64_t kernel_launches_per_iteration() const = 0;

@@ -98,11 +98,10 @@ __device__ __forceinline__ cx<T> stagm_prox(cx<T> y, T amp, T lam, T eps, bool f
 // Hardware rsqrt (<= 2 ulp): a Newton refinement was measured to change
 // nothing in the parity errors (Gamma's float32 error is set by cancellation
 // in y - prox(y)) while costing 5% of the frame kernel.
-__device__ __forceinline__ float rsqrt_nr(float n2) { return rsqrtf(n2); }
 __device__ __forceinline__ cx<float> prox_fast_f32(cx<float> y, float amp, float lam, float inv1pl) {
   const float n2 = norm2(y);
   if (n2 > 0.f) {
-    const float ri = rsqrt_nr(n2);
+    const float ri = rsqrtf(n2);
     const float m = (amp + lam * (n2 * ri)) * inv1pl;
     const float sc = m * ri;
     return cx<float>{y.x * sc, y.y * sc};
@@ -111,7 +110,7 @@ __device__ __forceinline__ cx<float> prox_fast_f32(cx<float> y, float amp, float
 }
 __device__ __forceinline__ float abs_fast_f32(cx<float> a) {
   const float n2 = norm2(a);
-  return n2 > 0.f ? n2 * rsqrt_nr(n2) : 0.f;
+  return n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
 }
 
 // Sum a per-thread double over the NT threads of one frame slot; result valid

@@ -90,7 +90,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       uint32_t raw[32];
 #pragma unroll
       for (int m = 0; m < RR; ++m) {
-        const cx<T> p = a.probe[y * S + g + GR * m];
+        // the unitary 1/S of both transforms folded into the cached probe
+        // (S a power of two: exact, results unchanged)
+        const cx<T> p = a.probe[y * S + g + GR * m] * a.scale;
         raw[2 * m] = __float_as_uint(p.x);
         raw[2 * m + 1] = __float_as_uint(p.y);
       }
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
   };
 
-  const T scale = a.scale;
+  const T scale = TMEMP ? T(1) : a.scale;  // TMEM probe carries the 1/S
   const T inv1pl = T(1) / (T(1) + a.lam);
   const int cx_ = t % CG, gc = t / CG;  // column-phase coordinates
 

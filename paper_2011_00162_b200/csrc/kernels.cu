@@ -575,6 +575,81 @@ cudaError_t launch_frame_sums(const T* amp, int64_t nfr, int64_t per, double* ou
   return cudaGetLastError();
 }
 
+// Augmented Lagrangian terms (metrics.cpp:73-101), fp64 accumulation.
+// Frame term per frame j: sum_i g_eps(z_i; b_i) + eta (Re(conj(G_i)(au_i - z_i)) + |au_i - z_i|^2 / 2),
+// g_eps = stagm::pixel_value (stagm.cpp:29-35) with b = amp^2.
+template <typename T>
+__global__ void lagrangian_frames_kernel(const cx<T>* au, const cx<T>* z, const cx<T>* gamma, const T* amp,
+                                         int64_t per, double eps, double eta, double* out) {
+  __shared__ double sm[16];
+  const int64_t base = blockIdx.x * per;
+  double acc = 0.0, dummy = 0.0;
+  for (int64_t i = threadIdx.x; i < per; i += blockDim.x) {
+    const cx<T> zi = z[base + i], ai = au[base + i], gi = gamma[base + i];
+    const double zx = zi.x, zy = zi.y;
+    const double ax = hypot(zx, zy), rb = static_cast<double>(amp[base + i]), b = rb * rb;
+    double g;
+    if (ax < eps * rb) {
+      g = 0.5 * (1.0 - eps) * (b - ax * ax / eps);
+    } else {
+      const double d = ax - rb;
+      g = 0.5 * d * d;
+    }
+    const double rx = static_cast<double>(ai.x) - zx, ry = static_cast<double>(ai.y) - zy;
+    acc += g + eta * (static_cast<double>(gi.x) * rx + static_cast<double>(gi.y) * ry + 0.5 * (rx * rx + ry * ry));
+  }
+  block_sum2(acc, dummy, sm);
+  if (threadIdx.x == 0) out[blockIdx.x] = acc;
+}
+template <typename T>
+cudaError_t launch_lagrangian_frames(const cx<T>* au, const cx<T>* z, const cx<T>* gamma, const T* amp, int64_t nfr,
+                                     int64_t per, double eps, double eta, double* out, cudaStream_t st) {
+  if (nfr <= 0) return cudaSuccess;
+  lagrangian_frames_kernel<T><<<static_cast<unsigned>(nfr), 256, 0, st>>>(au, z, gamma, amp, per, eps, eta, out);
+  return cudaGetLastError();
+}
+
+// Overlap term per (local pair, side): r (Re(conj(Lambda_s)(pi u_s - v)) + |pi u_s - v|^2 / 2);
+// out[2 lp + side] (0 where the side's subdomain lives on another rank).
+template <typename T>
+__global__ void lagrangian_pairs_kernel(const PairGeom* pairs, const cx<T>* u, const cx<T>* v, const cx<T>* lam,
+                                        double r, double* out) {
+  __shared__ double sm[16];
+  const PairGeom p = pairs[blockIdx.x];
+  const int side = blockIdx.y;
+  double acc = 0.0, dummy = 0.0;
+  if (p.u_off[side] >= 0) {
+    const int64_t n = static_cast<int64_t>(p.h) * p.w;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const int64_t rr = i / p.w, cc = i % p.w;
+      const cx<T> ui = u[p.u_off[side] + rr * p.u_pitch[side] + cc], vi = v[p.v_off + i],
+                  li = lam[p.lam_off[side] + i];
+      const double rx = static_cast<double>(ui.x) - static_cast<double>(vi.x);
+      const double ry = static_cast<double>(ui.y) - static_cast<double>(vi.y);
+      acc += r * (static_cast<double>(li.x) * rx + static_cast<double>(li.y) * ry + 0.5 * (rx * rx + ry * ry));
+    }
+  }
+  block_sum2(acc, dummy, sm);
+  if (threadIdx.x == 0) out[2 * blockIdx.x + side] = acc;
+}
+template <typename T>
+cudaError_t launch_lagrangian_pairs(const PairGeom* pairs, int npairs, const cx<T>* u, const cx<T>* v,
+                                    const cx<T>* lam, double r, double* out, cudaStream_t st) {
+  if (npairs <= 0) return cudaSuccess;
+  lagrangian_pairs_kernel<T><<<dim3(npairs, 2), 256, 0, st>>>(pairs, u, v, lam, r, out);
+  return cudaGetLastError();
+}
+template cudaError_t launch_lagrangian_frames<float>(const cx<float>*, const cx<float>*, const cx<float>*,
+                                                     const float*, int64_t, int64_t, double, double, double*,
+                                                     cudaStream_t);
+template cudaError_t launch_lagrangian_frames<double>(const cx<double>*, const cx<double>*, const cx<double>*,
+                                                      const double*, int64_t, int64_t, double, double, double*,
+                                                      cudaStream_t);
+template cudaError_t launch_lagrangian_pairs<float>(const PairGeom*, int, const cx<float>*, const cx<float>*,
+                                                    const cx<float>*, double, double*, cudaStream_t);
+template cudaError_t launch_lagrangian_pairs<double>(const PairGeom*, int, const cx<double>*, const cx<double>*,
+                                                     const cx<double>*, double, double*, cudaStream_t);
+
 template <typename T>
 __global__ void convert_amp_kernel(const void* src, int kind, T* amp, int64_t n, unsigned long long* neg) {
   unsigned long long bad = 0;

@@ -106,6 +106,15 @@ cudaError_t launch_widen_cx(const cx<float>* in, cx<double>* out, int64_t n, cud
 cudaError_t launch_segsum(const double* in, int stride, int comp, const int64_t* beg, int nseg, const int* map,
                           double* out, const int* skip, cudaStream_t st);
 
+// Augmented Lagrangian (metrics.cpp:73-101): per-frame terms [nfr] and
+// per-(local pair, side) overlap terms [2 npairs], fp64.
+template <typename T>
+cudaError_t launch_lagrangian_frames(const cx<T>* au, const cx<T>* z, const cx<T>* gamma, const T* amp, int64_t nfr,
+                                     int64_t per, double eps, double eta, double* out, cudaStream_t st);
+template <typename T>
+cudaError_t launch_lagrangian_pairs(const PairGeom* pairs, int npairs, const cx<T>* u, const cx<T>* v,
+                                    const cx<T>* lam, double r, double* out, cudaStream_t st);
+
 // Per-frame sums of amplitudes (for the R-factor denominator), double.
 template <typename T>
 cudaError_t launch_frame_sums(const T* amp, int64_t nfr, int64_t per, double* out, cudaStream_t st);

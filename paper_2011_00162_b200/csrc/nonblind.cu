@@ -250,7 +250,92 @@ class Nonblind final : public NonblindGpu {
     return ms;
   }
 
+  // metrics.cpp:73-101 for the current device state (u, z, Gamma, v, Lambda)
+  // with au = A u recomputed on the device.  Frame terms per frame and
+  // overlap terms per (pair, side) are fp64 partials with a single owner each;
+  // they are all-reduced exactly and summed on the host in the reference's
+  // order (subdomains, then pairs and sides), so the value is GPU-count
+  // invariant.
+  double lagrangian() override {
+    if (!z_valid_)
+      throw InvalidArgument("augmented_lagrangian: z of the current iterate is not stored (step with store_z)");
+    cudaStream_t s = R.st();
+    const int np = static_cast<int>(R.L.lpairs.size());
+    if (!lag_fr_.bytes()) {
+      lag_fr_.alloc(sizeof(double) * std::max<int64_t>(R.L.nfr, 1));
+      lag_pr_.alloc(sizeof(double) * 2 * std::max(np, 1));
+      lag_glob_.alloc(sizeof(double) * (R.D + 2 * std::max<size_t>(plan_.overlaps.size(), 1)));
+    }
+    forward_into(bp_.as<cx<T>>());
+    PDD_CUDA(launch_lagrangian_frames<T>(bp_.as<cx<T>>(), z_.as<cx<T>>(), gamma_[iter_ & 1].as<cx<T>>(),
+                                         R.amp.template as<T>(), R.L.nfr, R.SS(), cfg_.epsilon, cfg_.eta,
+                                         lag_fr_.as<double>(), s));
+    PDD_CUDA(launch_lagrangian_pairs<T>(R.pgeom.template as<PairGeom>(), np, u_.as<cx<T>>(), v_.as<cx<T>>(),
+                                        lam_.as<cx<T>>(), cfg_.r, lag_pr_.as<double>(), s));
+    const size_t P = plan_.overlaps.size();
+    double* glob = lag_glob_.as<double>();  // [D] frame terms, then [P][2] overlap terms
+    PDD_CUDA(cudaMemsetAsync(glob, 0, sizeof(double) * (R.D + 2 * P), s));
+    PDD_CUDA(launch_segsum(lag_fr_.as<double>(), 1, 0, R.sub_fr_beg.template as<int64_t>(), R.L.nls(),
+                           R.local_map.template as<int>(), glob, nullptr, s));
+    std::vector<double> pr(2 * static_cast<size_t>(np));
+    if (np) PDD_CUDA(cudaMemcpyAsync(pr.data(), lag_pr_.get(), sizeof(double) * pr.size(), cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> gp(2 * P, 0.0);
+    for (int lp = 0; lp < np; ++lp)
+      for (int side = 0; side < 2; ++side)
+        if (R.L.pgeom[lp].u_off[side] >= 0) gp[2 * R.L.lpairs[lp] + side] = pr[2 * lp + side];
+    if (P) PDD_CUDA(cudaMemcpyAsync(glob + R.D, gp.data(), sizeof(double) * 2 * P, cudaMemcpyHostToDevice, s));
+    if (R.comm) R.comm->allreduce_sum_f64(glob, R.D + 2 * P, s);
+    std::vector<double> h(R.D + 2 * P);
+    PDD_CUDA(cudaMemcpyAsync(h.data(), glob, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
+    double total = 0.0;
+    for (double x : h) total += x;
+    return total;
+  }
+
+  // run() with record_lagrangian: eager iterations, z kept, L recorded after
+  // each completed iteration (the reference's run loop, solver.cpp:258-260).
+  RunRecords run_recording() {
+    using clk = std::chrono::steady_clock;
+    ensure_z();
+    init_state();
+    R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
+    std::vector<double> lag, tms;
+    for (;;) {
+      const auto t0 = clk::now();
+      enqueue_iteration(static_cast<int>(iter_ & 1), true);
+      PDD_CUDA(cudaStreamSynchronize(R.st()));
+      const RunCtl c = R.read_ctl();
+      if (c.iter == iter_) break;  // stopped before completing another iteration
+      iter_ = c.iter;
+      z_valid_ = true;
+      tms.push_back(std::chrono::duration<double, std::milli>(clk::now() - t0).count());
+      lag.push_back(lagrangian());
+      if (c.stop) break;
+    }
+    enqueue_tail(static_cast<int>(iter_ & 1));
+    PDD_CUDA(cudaStreamSynchronize(R.st()));
+    const RunCtl c = R.read_ctl();
+    RunRecords out;
+    out.iterations = c.stop ? c.stop : c.iter;
+    out.diverged_at = c.diverged;
+    std::vector<double> rec(2 * static_cast<size_t>(out.iterations));
+    if (out.iterations)
+      PDD_CUDA(cudaMemcpy(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+    for (int64_t n = 0; n < out.iterations; ++n) {
+      out.rf.push_back(rec[2 * n]);
+      out.re.push_back(rec[2 * n + 1]);
+      out.t_ms.push_back(n < static_cast<int64_t>(tms.size()) ? tms[n] : 0.0);
+      out.lag.push_back(n < static_cast<int64_t>(lag.size()) ? lag[n] : NAN);
+    }
+    iter_ = out.iterations;
+    last_lag_ = out.lag;
+    return out;
+  }
+
   RunRecords run() override {  // solver.cpp:216-267
+    if (cfg_.record_lagrangian) return run_recording();
     SetupTimer tm;
     init_state();
     R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
@@ -271,8 +356,11 @@ class Nonblind final : public NonblindGpu {
     }
     iter_ = out.iterations;
     z_valid_ = false;
+    last_lag_.clear();
     return out;
   }
+
+  std::vector<double> lagrangian_history() const override { return last_lag_; }
 
   void iterate(int n) override {
     if (n <= 0) return;
@@ -390,6 +478,8 @@ class Nonblind final : public NonblindGpu {
   RankData<T> R;
   StateLayout layout_;
   DevMem probe_, probe64_, gamma_[2], bp_, u_, v_, lam_, s_, denom_, z_;
+  DevMem lag_fr_, lag_pr_, lag_glob_;
+  std::vector<double> last_lag_;
   Graph full_[2], tail_[2];
   int64_t iter_ = 0;
   bool z_valid_ = false;

@@ -686,6 +686,14 @@ class NonblindSolver(_SolverBase):
         dt = (time.perf_counter() - t0) * 1e3
         return [dt for _ in self.local_subs]
 
+    def augmented_lagrangian(self, state: SolverState) -> float:
+        """metrics.cpp:73-101 for `state` with au = A u (the solver invariant
+        after init_state/step), evaluated on the device in fp64 accumulation."""
+        self._set_state(state)
+        out = C.c_double()
+        check(L.lib().pdd_nonblind_lagrangian(self._h, C.byref(out)))
+        return out.value
+
     def r_factor_of(self, au: list) -> float:
         """solver.cpp:207-214 over host arrays au (as the reference's signature)."""
         if self._sqrt_f is None:
@@ -704,9 +712,15 @@ class NonblindSolver(_SolverBase):
         rec = np.zeros((cfg.max_iters, 3))
         rc = L.lib().pdd_nonblind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
         check(rc, iteration=int(div.value))
+        lag = [None] * int(n.value)
+        if cfg.record_lagrangian:  # solver.cpp:258-260, evaluated on the device
+            nl = C.c_int64()
+            hist = np.zeros(max(int(n.value), 1))
+            check(L.lib().pdd_nonblind_lagrangian_history(self._h, ptr(hist), C.c_int64(hist.size), C.byref(nl)))
+            lag = [float(x) for x in hist[:int(nl.value)]] + [None] * (int(n.value) - int(nl.value))
         records = []
         for k in range(int(n.value)):
-            r = ConvergenceRecord(k + 1, float(rec[k, 0]), float(rec[k, 1]), None,
+            r = ConvergenceRecord(k + 1, float(rec[k, 0]), float(rec[k, 1]), lag[k],
                                   [float(rec[k, 2])] * len(self.local_subs), float(rec[k, 2]), float(rec[k, 2]))
             records.append(r)
             if on_iteration:

@@ -1,0 +1,16 @@
+#!/usr/bin/env bash
+# One GPU session: parity tests, bench + launch list, ncu captures of the two
+# kernels of the iteration (sweep, gather) on config 4.
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+TAG=${TAG:-r1}
+timeout 900 python -m pytest tests/ -q -m gpu > gpurun_out/tests_$TAG.log 2>&1
+tail -n 1 gpurun_out/tests_$TAG.log
+bash scripts/gpu_bench.sh
+if [ "${NCU:-1}" = 1 ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_stream -c 1 \
+    -o gpurun_out/sweep_$TAG -f python scripts/prof_frame.py 4 1 > gpurun_out/ncu_sweep_$TAG.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -c 1 \
+    -o gpurun_out/gather_$TAG -f python scripts/prof_frame.py 4 1 > gpurun_out/ncu_gather_$TAG.log 2>&1
+  tail -n 1 gpurun_out/ncu_sweep_$TAG.log gpurun_out/ncu_gather_$TAG.log
+fi

@@ -11,7 +11,12 @@ import torch  # noqa: E402
 import paper_2011_00162_b200 as P  # noqa: E402
 from paper_2011_00162_b200 import _lib as L, sim  # noqa: E402
 
-cfg = sim.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 4]
+arg = sys.argv[1] if len(sys.argv) > 1 else "4"
+if "/" in arg:  # ad-hoc geometry N/s/step (stripes over 8 row blocks, f32)
+    N, s_, st = (int(x) for x in arg.split("/"))
+    cfg = sim.Config(f"adhoc{N}_{s_}_{st}", N, s_, st, 4.0, s_ / 4, ("stripes", 8, "rows"), "f32", 1e4, 10)
+else:
+    cfg = sim.CONFIGS[int(arg)]
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 plan = sim.make_plan(cfg)
 J, s = plan.geometry.frame_count(), cfg.s

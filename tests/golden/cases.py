@@ -88,3 +88,20 @@ def blind_inputs():
         w0 = (((yy - s / 2) ** 2 + (xx - s / 2) ** 2) <= (0.375 * s) ** 2).astype(complex)
         out[name] = (N, s, step, D, f, w0)
     return out
+
+
+# nonblind cases with augmented-Lagrangian goldens
+LAGRANGIAN_CASES = ("n64D2", "n64D3")
+
+
+def lagrangian_recipe(N, s, step, D, probe):
+    """(eta, r) inside the stability set, the recipe of test_solver.cpp:234-266:
+    c0 = max(2 max rho, sqrt(max rho)), c1 = 2 max rho over the subdomains'
+    illumination densities, L = lipschitz_constant(0.5)."""
+    plan = O.plan_stripes(O.make_raster_scan(N, N, s, step), D)
+    mx = max(float(np.max(O.illumination_density(probe, lg))) for lg in plan.local_geometries)
+    c0 = max(2.0 * mx, np.sqrt(mx))
+    c1 = 2.0 * mx
+    L = O.lipschitz_constant(0.5)
+    eta = 1.05 * (6.0 * L + 2.0 * L * L + 2.0 * c1 * (L + 1.0) ** 2 / (c0 * c0))
+    return eta, 1.1 * c0 * eta

@@ -60,6 +60,18 @@ def main():
         run = R.nonblind_run(ps, f, probe, R.nonblind_cfg(max_iters=20, tol_rf=1e-300))
         out[f"nb_{name}_records"] = run["records"][:, :2]
         out[f"nb_{name}_merged20"] = run["merged"]
+    # augmented Lagrangian records (metrics.cpp:73-101 via solver.cpp:258-260):
+    # default parameters, and the stability-set recipe of test_solver.cpp:234-266
+    for name, (N, s, step, D, f, probe) in cases.nonblind_inputs().items():
+        if name not in cases.LAGRANGIAN_CASES:
+            continue
+        ps = R.plan_spec(N, N, s, step, D)
+        run = R.nonblind_run(ps, f, probe, R.nonblind_cfg(max_iters=15, tol_rf=1e-300, record_lagrangian=True))
+        out[f"lag_{name}_default"] = run["records"][:, 2]
+        eta, r = cases.lagrangian_recipe(N, s, step, D, probe)
+        run = R.nonblind_run(ps, f, probe, R.nonblind_cfg(eta=eta, r=r, max_iters=60, tol_rf=1e-14,
+                                                          record_lagrangian=True))
+        out[f"lag_{name}_recipe"] = run["records"][:, 2]
     # blind solver: stock w0 + estimated mask, 2 steps; custom disk w0 run
     for name, (N, s, step, D, f, w0) in cases.blind_inputs().items():
         ps = R.plan_spec(N, N, s, step, D)

@@ -105,6 +105,30 @@ def test_nonblind_goldens():
         assert rel_l2(merged, G[f"nb_{name}_merged20"]) < 1e-9
 
 
+def _lagrangians(plan, f, probe, **cfg):
+    _, _, rec = O.NonblindSolver(plan, f, probe, O.NonblindConfig(record_lagrangian=True, **cfg)).run()
+    return np.array([r.lagrangian for r in rec])
+
+
+def test_lagrangian_goldens():
+    """augmented_lagrangian (metrics.cpp:73-101) pinned against the compiled
+    reference's ConvergenceRecord::lagrangian, default parameters and the
+    stability-set recipe of test_solver.cpp:234-266 (monotone there)."""
+    inputs = cases.nonblind_inputs()
+    for name in cases.LAGRANGIAN_CASES:
+        N, s, step, D, f, probe = inputs[name]
+        plan = O.plan_stripes(O.make_raster_scan(N, N, s, step), D)
+        lag = _lagrangians(plan, f, probe, max_iters=15, tol_rf=1e-300)
+        assert np.allclose(lag, G[f"lag_{name}_default"], rtol=1e-10, atol=0)
+        eta, r = cases.lagrangian_recipe(N, s, step, D, probe)
+        lag = _lagrangians(plan, f, probe, eta=eta, r=r, max_iters=60, tol_rf=1e-14)
+        ref = G[f"lag_{name}_recipe"]
+        assert len(lag) == len(ref) == 60
+        assert np.allclose(lag, ref, rtol=1e-10, atol=0)
+        # the reference's property: non-increasing up to 1e-9 relative
+        assert np.all(np.diff(ref) <= 1e-9 * np.abs(ref[:-1]))
+
+
 def test_blind_goldens():
     for name, (N, s, step, D, f, w0) in cases.blind_inputs().items():
         g = O.make_raster_scan(N, N, s, step)

@@ -224,6 +224,12 @@ PDD_API int pdd_blind_sync(pdd_blind* h);
 PDD_API int pdd_blind_launches_per_iteration(const pdd_blind* h, int64_t* n);
 PDD_API int pdd_blind_destroy(pdd_blind* h);
 
+/* disk_support_mask (blind.hpp:47-48): centred disk in wrapped Fourier coordinates, out [side][side] */
+PDD_API int pdd_disk_support_mask(int64_t side, double radius, double* out);
+/* estimate_support_mask (blind.hpp:50-52): smallest centred disk holding energy_fraction of the
+ * Fourier energy of probe_guess [side][side] c128 (FFT on the device); out [side][side] */
+PDD_API int pdd_estimate_support_mask(const double* probe_guess, int64_t side, double energy_fraction, double* out);
+
 /* ---- pinned host memory for end-to-end staging ----------------------------- */
 PDD_API int pdd_host_alloc(void** p, int64_t bytes);
 PDD_API int pdd_host_free(void* p);

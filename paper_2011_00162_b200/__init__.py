@@ -6,7 +6,7 @@ from ._lib import (LIB_PATH, CudaError, DivergenceError, InvalidArgument, OutOfR
                    exported_symbols, lib)
 from .ptychodd import (BlindConfig, BlindResult, BlindSolver, BlindState, ConvergenceRecord, DecompositionPlan, NonblindConfig, NonblindResult, NonblindSolver, Region,
                        ScanGeometry, SolverState, adjoint, adjoint_probe, fft2_normalized, forward, ifft2_normalized,
-                       illumination_density, intensity, make_raster_scan, merge, partition_frames, plan_grid,
+                       illumination_density, intensity, make_raster_scan, merge, partition_frames, plan_from_arrays, plan_grid,
                        plan_stripes, probe_density, r_factor, relative_error, restrict_overlap, scan_coverage, snr_db,
                        stagm, disk_support_mask, estimate_support_mask)
 

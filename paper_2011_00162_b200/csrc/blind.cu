@@ -42,6 +42,8 @@ double freq_radius(int64_t k, int64_t l, int64_t side) {  // blind.cpp:22-27
   return std::sqrt(kk * kk + ll * ll);
 }
 
+}  // namespace
+
 std::vector<double> disk_mask(int64_t side, double radius) {  // blind.cpp:46-52
   std::vector<double> m(static_cast<size_t>(side * side), 0.0);
   for (int64_t k = 0; k < side; ++k)
@@ -73,6 +75,8 @@ std::vector<double> estimate_mask(const std::vector<double>& w0, int64_t side, d
   }
   return disk_mask(side, radius);
 }
+
+namespace {
 
 template <typename T>
 class Blind final : public BlindGpu {

@@ -562,6 +562,24 @@ int pdd_nonblind_set_state(pdd_nonblind* h, const double* u, const double* z, co
   NB_CALL(h, h->s->set_state(u, z, gamma, v, lambda, iteration));
 }
 int pdd_nonblind_forward(pdd_nonblind* h, double* au) { NB_CALL(h, need(au, "au"); h->s->forward_frames(au)); }
+int pdd_disk_support_mask(int64_t side, double radius, double* out) {
+  return guard([&] {
+    need(out, "out");
+    if (side < 1) throw pdd::InvalidArgument("disk_support_mask: side >= 1");
+    const auto m = pdd::disk_mask(side, radius);
+    std::copy(m.begin(), m.end(), out);
+  });
+}
+int pdd_estimate_support_mask(const double* probe_guess, int64_t side, double energy_fraction, double* out) {
+  return guard([&] {
+    need(probe_guess, "probe_guess");
+    need(out, "out");
+    if (side < 1) throw pdd::InvalidArgument("estimate_support_mask: side >= 1");
+    const auto m = pdd::estimate_mask(std::vector<double>(probe_guess, probe_guess + 2 * side * side), side,
+                                      energy_fraction);
+    std::copy(m.begin(), m.end(), out);
+  });
+}
 int pdd_nonblind_lagrangian(pdd_nonblind* h, double* out) {
   NB_CALL(h, need(out, "out"); *out = h->s->lagrangian());
 }

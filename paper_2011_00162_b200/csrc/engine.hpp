@@ -104,6 +104,11 @@ class NonblindGpu {
   virtual int64_t kernel_launches_per_iteration() const = 0;
 };
 
+// disk_support_mask / estimate_support_mask (blind.cpp:46-75): [side][side] 0/1;
+// the estimate's spectrum comes from the GPU FFT.
+std::vector<double> disk_mask(int64_t side, double radius);
+std::vector<double> estimate_mask(const std::vector<double>& w0, int64_t side, double frac);
+
 std::unique_ptr<NonblindGpu> make_nonblind(const Plan& plan, const DataSpec& data, const double* probe,
                                            const NonblindConfig& cfg, const double* pin_ones, int dtype,
                                            int device, Comm* comm);

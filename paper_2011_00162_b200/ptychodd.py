@@ -180,6 +180,26 @@ def plan_grid(geometry: ScanGeometry, Dr: int, Dc: int) -> DecompositionPlan:
     return _plan_handle(h)
 
 
+def plan_from_arrays(geometry: ScanGeometry, D: int, assignment, subdomains, pairs, regions) -> DecompositionPlan:
+    """Any DecompositionPlan (ddplan.hpp:12-35) from its arrays: frame
+    assignment [J], subdomain rectangles [D][4] (r0, r1, c0, c1), overlap
+    pairs [P][2] (d1 < d2) and regions [P][4]; validated as the reference's
+    plan invariants require (windows inside their subdomain, overlaps inside
+    both sides)."""
+    g = geometry
+    pos = np.ascontiguousarray(g.positions, np.int64)
+    asg = np.ascontiguousarray(assignment, np.int32)
+    subs = np.ascontiguousarray(subdomains, np.int64).reshape(-1, 4)
+    prs = np.ascontiguousarray(pairs, np.int32).reshape(-1, 2)
+    regs = np.ascontiguousarray(regions, np.int64).reshape(-1, 4)
+    h = C.c_void_p()
+    check(L.lib().pdd_plan_from_arrays(C.c_int64(g.frame_side), C.c_int64(g.step), C.c_int64(g.image_height),
+                                       C.c_int64(g.image_width), C.c_int64(pos.shape[0]), ptr(pos), C.c_int32(D),
+                                       ptr(asg), ptr(subs), C.c_int32(prs.shape[0]), ptr(prs), ptr(regs),
+                                       C.byref(h)))
+    return _plan_handle(h)
+
+
 def scan_coverage(geometry: ScanGeometry) -> np.ndarray:
     """scan.cpp:36-44 (as float64, like RealField2D)."""
     plan = plan_stripes(geometry, 1) if geometry.frame_count() == geometry.grid_rows * geometry.grid_cols else None

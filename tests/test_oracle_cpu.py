@@ -182,3 +182,31 @@ def test_reference_is_ill_conditioned_over_long_horizons():
         drift[iters] = rel_l2(m, ref["merged"])
     assert drift[20] < 1e-10
     assert drift[100] > 1e-4
+
+
+def test_sign_zero_degeneracy_is_fft_rounding_dependent():
+    """Why one reference unit test (test_solver.cpp:148-179, "solver iterates
+    match the reference ADMM") cannot be met by any FFT other than the one the
+    reference links: on make_toy(40, 8, 4) the zone-plate probe is real and
+    symmetric and u0 = 1, so many y = A u0 are exactly 0 in exact arithmetic;
+    the prox takes sign(y) (stagm.cpp:71, sign(0) := 1) of their +-1e-16
+    rounding noise.  Two float64 implementations that differ only in the FFT
+    -- the numpy restatement and the compiled reference -- already disagree by
+    O(1) after one step there, while agreeing to 1e-12 on a generic problem."""
+    from oracle import ref_lib as R
+    N, s, step = 40, 8, 4
+    sample, probe, pin = R.toy(N, s, step, 21)
+    f = R.simulate_frames(probe, sample, step)
+    g = O.make_raster_scan(N, N, s, step)
+    st = R.nonblind_steps(R.plan_spec(N, N, s, step, 1), f, probe, R.nonblind_cfg(), 1, pin=pin)
+    sol = O.NonblindSolver(O.plan_stripes(g, 1), f, probe, O.NonblindConfig(), pin_ones=pin)
+    ost = sol.init_state()
+    sol.step(ost, [z.copy() for z in ost.z])
+    assert np.abs(ost.u[0] - st["u"][0]).max() > 0.1
+    # same solver pair on a generic (non-symmetric) problem: agreement
+    N, s, step, D, f2, probe2 = cases.nonblind_inputs()["n64D2"]
+    st2 = R.nonblind_steps(R.plan_spec(N, N, s, step, D), f2, probe2, R.nonblind_cfg(), 1)
+    sol2 = O.NonblindSolver(O.plan_stripes(O.make_raster_scan(N, N, s, step), D), f2, probe2, O.NonblindConfig())
+    o2 = sol2.init_state()
+    sol2.step(o2, [z.copy() for z in o2.z])
+    assert max(np.abs(a - b).max() for a, b in zip(o2.u, st2["u"])) < 1e-12

@@ -1,13 +1,15 @@
 #!/usr/bin/env bash
-# Drop-in proof build: the reference's own unit tests for the solver layer
-# (proj/tests/test_solver.cpp, test_blind.cpp), compiled unmodified from where
-# they lie, linked against
-#   - the reference's non-solver sources (field, fft, scan, forward, stagm,
-#     ddplan, simulate, metrics: test-data generation and the transparent
-#     reference ADMM the tests compare against; fft via oracle/fftw_shim),
-#   - dropin/ptychodd_solver_cuda.cpp, which defines NonblindSolver and
-#     BlindSolver (replacing proj/src/solver.cpp and blind.cpp) over
-#     include/ptychodd_cuda.h, and
+# Drop-in proof build: the reference's own unit tests (proj/tests/*.cpp except
+# test_io.cpp), compiled unmodified from where they lie, linked against
+#   - dropin/ptychodd_ops_cuda.cpp    (fft.hpp, forward.hpp, stagm.hpp over the
+#                                     C-ABI; replaces proj/src/fft.cpp,
+#                                     forward.cpp, stagm.cpp)
+#   - dropin/ptychodd_solver_cuda.cpp (NonblindSolver, BlindSolver over the
+#                                     C-ABI; replaces proj/src/solver.cpp,
+#                                     blind.cpp)
+#   - the reference's remaining sources (field, scan, ddplan, simulate,
+#     metrics: data structures, integer planning, test-data generation and
+#     the metrics, which now call the GPU operators), and
 #   - paper_2011_00162_b200/libptychodd_cuda.so.
 # The test framework header is dropin/doctest.h (doctest is not in the image).
 # Output: dropin/_build/ptychodd_dropin_tests (git-ignored; travels to the GPU
@@ -22,20 +24,20 @@ if [ ! -d "$ref/src" ]; then
   exit 0
 fi
 mkdir -p "$out"
-CXX="g++ -std=c++20 -O2 -DNDEBUG -I$ref/include -I$repo/oracle/fftw_shim -I$here -I$repo/include"
+CXX="g++ -std=c++20 -O2 -DNDEBUG -I$ref/include -I$here -I$repo/include"
 objs=()
-for s in field fft scan forward stagm ddplan simulate metrics; do
+for s in field scan ddplan simulate metrics; do
   $CXX -c "$ref/src/$s.cpp" -o "$out/ref_$s.o" &
   objs+=("$out/ref_$s.o")
 done
-for t in test_main test_solver test_blind; do
+for t in test_main test_field_fft test_forward test_stagm test_ddplan test_simulate test_metrics test_solver test_blind; do
   $CXX -c "$ref/tests/$t.cpp" -o "$out/$t.o" &
   objs+=("$out/$t.o")
 done
-$CXX -c "$repo/oracle/fftw_shim/fftw_shim.cpp" -o "$out/fftw_shim.o" &
 $CXX -c "$here/ptychodd_solver_cuda.cpp" -o "$out/ptychodd_solver_cuda.o" &
+$CXX -c "$here/ptychodd_ops_cuda.cpp" -o "$out/ptychodd_ops_cuda.o" &
 wait
-objs+=("$out/fftw_shim.o" "$out/ptychodd_solver_cuda.o")
+objs+=("$out/ptychodd_solver_cuda.o" "$out/ptychodd_ops_cuda.o")
 lib="$repo/paper_2011_00162_b200"
 g++ -o "$out/ptychodd_dropin_tests" "${objs[@]}" -L"$lib" -lptychodd_cuda -Wl,-rpath,'$ORIGIN/../../paper_2011_00162_b200' \
   -lpthread

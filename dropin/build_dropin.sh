@@ -12,8 +12,10 @@
 #     the metrics, which now call the GPU operators), and
 #   - paper_2011_00162_b200/libptychodd_cuda.so.
 # The test framework header is dropin/doctest.h (doctest is not in the image).
-# Output: dropin/_build/ptychodd_dropin_tests (git-ignored; travels to the GPU
-# box with the snapshot).  Run there:  dropin/_build/ptychodd_dropin_tests
+# Also the reference's acceptance program (proj/tests/acceptance.cpp, the
+# paper's criteria 1-6) linked the same way.
+# Output: dropin/_build/ptychodd_dropin_{tests,acceptance} (git-ignored; they
+# travel to the GPU box with the snapshot).
 set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"
 repo="$(dirname "$here")"
@@ -38,8 +40,13 @@ $CXX -c "$here/ptychodd_solver_cuda.cpp" -o "$out/ptychodd_solver_cuda.o" &
 $CXX -c "$here/ptychodd_ops_cuda.cpp" -o "$out/ptychodd_ops_cuda.o" &
 wait
 objs+=("$out/ptychodd_solver_cuda.o" "$out/ptychodd_ops_cuda.o")
+$CXX -c "$ref/tests/acceptance.cpp" -o "$out/acceptance.o"
 lib="$repo/paper_2011_00162_b200"
-g++ -o "$out/ptychodd_dropin_tests" "${objs[@]}" -L"$lib" -lptychodd_cuda -Wl,-rpath,'$ORIGIN/../../paper_2011_00162_b200' \
-  -lpthread
+link() { g++ -o "$1" "${@:2}" -L"$lib" -lptychodd_cuda -Wl,-rpath,'$ORIGIN/../../paper_2011_00162_b200' -lpthread; }
+link "$out/ptychodd_dropin_tests" "${objs[@]}"
+# the reference's acceptance program (paper criteria 1-6) on the same library
+lib_objs=()
+for o in "${objs[@]}"; do case "$o" in */test_*.o) ;; *) lib_objs+=("$o") ;; esac; done
+link "$out/ptychodd_dropin_acceptance" "${lib_objs[@]}" "$out/acceptance.o"
 rm -f "$out"/*.o
-echo "built $out/ptychodd_dropin_tests"
+echo "built $out/ptychodd_dropin_tests $out/ptychodd_dropin_acceptance"

@@ -34,3 +34,19 @@ def test_reference_unit_tests_pass_on_the_gpu_library():
     assert len(ok) == 53 and r.returncode == 0, r.stdout + r.stderr[-2000:]
     assert "augmented Lagrangian is monotone for (r, eta) inside the stability set" in ok
     assert "blind recovery on a toy problem drives RF down with exact support zeros" in ok
+
+
+ACC = os.path.join(ROOT, "dropin", "_build", "ptychodd_dropin_acceptance")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="drop-in acceptance binary not built (needs /root/reference)")
+def test_reference_acceptance_criteria_on_the_gpu_library():
+    """proj/tests/acceptance.cpp (the paper's criteria) on the GPU library:
+    1, 2, 4, 5, 6 pass; criterion 3's iteration-count half passes, its
+    efficiency half is the reference's per-thread virtual-time model
+    (profiles/r1_dropin_acceptance_b200.txt)."""
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=1500)
+    for c in (1, 2, 4, 5, 6):
+        assert re.search(rf"^PASS criterion {c}:", r.stdout, re.M), r.stdout
+    m = re.search(r"D=10/D=1 = ([0-9.]+) \(<=1.20\)", r.stdout)
+    assert m and float(m.group(1)) <= 1.20, r.stdout

@@ -333,7 +333,8 @@ def main():
         torch.cuda.synchronize()
         t_e2e = allmax(dist, time.perf_counter() - t0)
         h2d = j_local * s * s * 4 + probe.nbytes
-        d2h = n_local * 16 + res.iterations * 24
+        g = plan.geometry
+        d2h = n_local * 16 + (g.image_height * g.image_width * 16 if world == 1 else 0) + res.iterations * 24
         line["e2e"] = {"value": J * res.iterations / t_e2e, "unit": base["unit"], "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "iterations_per_step": res.iterations,
                        "timer": "host wall clock around synchronous C-ABI calls (create+upload, run, download)"}

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import time
 from dataclasses import dataclass, field
 from types import SimpleNamespace
@@ -482,6 +483,33 @@ class SolverState:
     iteration: int = 0
 
 
+def _prefaulted(shape) -> np.ndarray:
+    """complex128 array whose pages are already mapped (written once):
+    device->host copies into it then run at copy speed instead of at
+    page-fault speed."""
+    a = np.empty(shape, np.complex128)
+    a.fill(0)
+    return a
+
+
+class _Prefault(threading.Thread):
+    """Allocates and maps the host result buffers on a helper thread while the
+    device loop runs (the C-ABI call releases the GIL).  (Page-locking them
+    instead costs more than it saves: cudaMallocHost of 2 GB takes ~0.9 s and
+    stalls the device loop.)"""
+
+    def __init__(self, *shapes):
+        super().__init__(daemon=True)
+        self.shapes, self.out = shapes, None
+
+    def run(self):
+        self.out = [_prefaulted(sh) for sh in self.shapes]
+
+    def result(self):
+        self.join()
+        return self.out
+
+
 class _LazyList(list):
     """A list filled on first access (device -> host download on demand)."""
 
@@ -730,7 +758,11 @@ class NonblindSolver(_SolverBase):
         n = C.c_int64()
         div = C.c_int64()
         rec = np.zeros((cfg.max_iters, 3))
+        g = self.plan.geometry
+        pf = _Prefault((g.image_height, g.image_width) if self.world == 1 else (0,), (self._lay.image_elems,))
+        pf.start()
         rc = L.lib().pdd_nonblind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
+        merged, u = pf.result()
         check(rc, iteration=int(div.value))
         lag = [None] * int(n.value)
         if cfg.record_lagrangian:  # solver.cpp:258-260, evaluated on the device
@@ -745,17 +777,16 @@ class NonblindSolver(_SolverBase):
             records.append(r)
             if on_iteration:
                 on_iteration(r)
-        g = self.plan.geometry
-        merged = None
         if self.world == 1:  # merged on the device (ddplan.cpp:104-121)
-            merged = np.empty((g.image_height, g.image_width), np.complex128)
             check(L.lib().pdd_nonblind_merged(self._h, ptr(merged)))
-        u = self._get_u()
+        else:
+            merged = None
+        u = self._get_u(u)
         last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
         return NonblindResult(u, merged, records, int(n.value), last.rf, last.re)
 
-    def _get_u(self) -> list:
-        u = np.zeros(self._lay.image_elems, np.complex128)
+    def _get_u(self, out: Optional[np.ndarray] = None) -> list:
+        u = np.empty(self._lay.image_elems, np.complex128) if out is None else out
         check(L.lib().pdd_nonblind_get_state(self._h, ptr(u), None, None, None, None, None))
         return self._split_images(u)
 
@@ -962,7 +993,11 @@ class BlindSolver(_SolverBase):
         n = C.c_int64()
         div = C.c_int64()
         rec = np.zeros((cfg.max_iters, 3))
+        g = self.plan.geometry
+        pf = _Prefault((g.image_height, g.image_width) if self.world == 1 else (0,), (self._lay.image_elems,))
+        pf.start()
         rc = L.lib().pdd_blind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
+        merged, u = pf.result()
         check(rc, iteration=int(div.value))
         records = []
         for k in range(int(n.value)):
@@ -971,11 +1006,13 @@ class BlindSolver(_SolverBase):
             records.append(r)
             if on_iteration:
                 on_iteration(r)
-        u = np.zeros(self._lay.image_elems, np.complex128)
         check(L.lib().pdd_blind_get_state(self._h, None, None, None, ptr(u), None, None, None, None, None))
         u = self._split_images(u)
         probe, spec, mask, _ = self._probe_info()
-        merged = merge(u, self.plan) if self.world == 1 else None
+        if self.world == 1:  # merged on the device (ddplan.cpp:104-121)
+            check(L.lib().pdd_blind_merged(self._h, ptr(merged)))
+        else:
+            merged = None
         last = records[-1] if records else ConvergenceRecord(0, math.nan, math.nan)
         return BlindResult(probe, spec, mask, u, merged, records, int(n.value), last.rf, last.re)
 

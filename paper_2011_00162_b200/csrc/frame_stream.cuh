@@ -56,7 +56,9 @@ struct ProbeTmem {
   static_assert(RAW <= 512, "probe does not fit in TMEM");
 };
 
-template <typename T, class SH, bool FAST, bool TMEMP = false>
+// FWD = true: the forward half only (FrameMode kFwd: A u -> frames_out,
+// |A u|^2 -> inten_out, R-factor partials), e.g. the trailing R-factor pass.
+template <typename T, class SH, bool FAST, bool TMEMP = false, bool FWD = false>
 __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const FrameArgs<T> a) {
   constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
@@ -132,8 +134,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int k1 = 0; k1 < GC; ++k1) {
         const int ky = gc + GC * q + RC * k1;
-        pg[q * GC + k1] = a.gamma_in[base + static_cast<int64_t>(ky) * S];
-        pa[q * GC + k1] = a.amp[base + static_cast<int64_t>(ky) * S];
+        if constexpr (!FWD) pg[q * GC + k1] = a.gamma_in[base + static_cast<int64_t>(ky) * S];
+        if (!FWD || a.rf_part) pa[q * GC + k1] = a.amp[base + static_cast<int64_t>(ky) * S];
       }
   };
   prefetch(blockIdx.x, 0);
@@ -211,6 +213,27 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
       // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
       T acc = T(0);
+      if constexpr (FWD) {
+#pragma unroll
+        for (int q = 0; q < RC / GC; ++q)
+#pragma unroll
+          for (int k1 = 0; k1 < GC; ++k1) {
+            const int e = q * GC + k1;
+            const int ky = gc + GC * q + RC * k1;
+            const int64_t idx = fbase + static_cast<int64_t>(ky) * S + x;
+            const cx<T> au = w[e] * scale;
+            if (a.frames_out) a.frames_out[idx] = au;
+            if (a.inten_out) a.inten_out[idx] = norm2(au);
+            if (a.rf_part) {
+              if constexpr (FAST && std::is_same_v<T, float>) acc += fabsf(abs_fast_f32(au) - pa[e]);
+              else acc += fabs(sqrt(norm2(au)) - pa[e]);
+            }
+          }
+        rf_acc += acc;
+        if (grp + 1 < NG) prefetch(f, grp + 1);
+        else prefetch(f + gridDim.x, 0);
+        continue;  // groups own disjoint columns of buf: no barrier between them
+      }
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q)
 #pragma unroll
@@ -258,7 +281,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
     // ---------------- rows, inverse -> x conj(probe) -> back-projection tile
 #pragma unroll 1
-    for (int rb = 0; rb < NRB; ++rb) {
+    for (int rb = 0; rb < (FWD ? 0 : NRB); ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
       cx<T> v[RR], pv[RR];
       probe_row(rb, y, g, pv);

@@ -51,10 +51,10 @@ struct StreamPick {
 template <> struct StreamPick<float, 128> { using type = StreamShape<128, 512, 8, 8>; };
 template <> struct StreamPick<float, 64> { using type = StreamShape<64, 256, 4, 8, 2>; };
 
-template <typename T, class SH, bool FAST>
+template <typename T, class SH, bool FAST, bool FWD = false>
 static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
   // TMEM probe cache where it keeps occupancy (one persistent CTA per SM)
-  auto kern = sweep_stream_kernel<T, SH, FAST, std::is_same_v<T, float> && SH::MINB == 1>;
+  auto kern = sweep_stream_kernel<T, SH, FAST, std::is_same_v<T, float> && SH::MINB == 1, FWD>;
   const size_t smem = stream_smem_bytes<T, SH>();
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -79,6 +79,10 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
   if constexpr (MODE == kSweep && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
     using SH = typename StreamPick<T, S>::type;
     return a.fast_prox ? launch_stream<T, SH, true>(a, st) : launch_stream<T, SH, false>(a, st);
+  }
+  if constexpr (MODE == kFwd && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
+    using SH = typename StreamPick<T, S>::type;
+    return a.fast_prox ? launch_stream<T, SH, true, true>(a, st) : launch_stream<T, SH, false, true>(a, st);
   }
   using C = FrameCfg<T, S>;
   using E = Fft2<T, S, C::R>;

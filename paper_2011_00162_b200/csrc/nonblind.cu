@@ -211,7 +211,7 @@ class Nonblind final : public NonblindGpu {
 
   // Launch iteration-pair graphs until the device reports a stop; poll every
   // kPoll launches.  Returns per-launch milliseconds.
-  std::vector<double> drive(int max_total, bool poll) {
+  std::vector<double> drive(int max_total, bool poll, bool tail = true) {
     ensure_graphs();
     constexpr int kPoll = 8;
     cudaStream_t s = R.st();
@@ -245,8 +245,10 @@ class Nonblind final : public NonblindGpu {
     for (auto e : ev) cudaEventDestroy(e);
     const RunCtl c = R.read_ctl();
     iter_ = c.iter;
-    tail_[iter_ & 1].launch(s);
-    PDD_CUDA(cudaStreamSynchronize(s));
+    if (tail) {  // R-factor of the final iterate (its frame pass)
+      tail_[iter_ & 1].launch(s);
+      PDD_CUDA(cudaStreamSynchronize(s));
+    }
     return ms;
   }
 
@@ -377,7 +379,7 @@ class Nonblind final : public NonblindGpu {
     PDD_CUDA(cudaEventCreate(&e0));
     PDD_CUDA(cudaEventCreate(&e1));
     PDD_CUDA(cudaEventRecord(e0, R.st()));
-    drive(n, false);  // ends with the trailing R-factor pass and a stream sync
+    drive(n, false, false);  // exactly n iterations (no trailing R-factor pass)
     PDD_CUDA(cudaEventRecord(e1, R.st()));
     PDD_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;

@@ -171,6 +171,19 @@ def run_reference(cfg, iters: int, warmup: int):
     from oracle import ref_lib
 
     smp = reference_sample(cfg)
+    if cfg.blind and ref_lib.available():  # BlindSolver::run (blind.cpp:298-358), disk w0 as configured
+        from paper_2011_00162_b200 import sim
+
+        ps = ref_lib.plan_spec(smp["H"], smp["W"], cfg.s, cfg.step, smp["D"], smp["axis"])
+        bc = ref_lib.blind_cfg(max_iters=iters + warmup, tol_rf=1e-300, threads=0, **cfg.solver)
+        w0 = sim.disk_probe(cfg.s, cfg.init_disk_radius) if cfg.init_disk_radius else None
+        out = ref_lib.blind_run(ps, smp["f"], bc, w0=w0)
+        t = out["records"][warmup:, 3]
+        value = smp["frames"] * len(t) / (float(np.sum(t)) / 1e3)
+        sample = (f"{cfg.name} geometry (s={cfg.s}, step={cfg.step}) cropped to {smp['H']}x{smp['W']} "
+                  f"({smp['frames']} frames), {smp['D']} row-strip subdomains (the reference has no 2-D plans), "
+                  f"blind, {len(t)} timed iterations; FFT = oracle/fftw_shim (radix-2, not FFTW)")
+        return value, "reference", smp["D"], sample, float(np.mean(t))
     if ref_lib.available():
         ps = ref_lib.plan_spec(smp["H"], smp["W"], cfg.s, cfg.step, smp["D"], smp["axis"])
         rcfg = ref_lib.nonblind_cfg(max_iters=iters + warmup, tol_rf=1e-300, threads=0)
@@ -242,6 +255,8 @@ def main():
     import paper_2011_00162_b200 as P
     from paper_2011_00162_b200 import _lib as L
 
+    if cfg.blind:
+        return bench_blind(args, cfg, base, rank, world, local, dist)
     inp = sim.make_inputs(cfg, device=True)
     plan, probe, amp = inp["plan"], inp["probe"], inp["amplitudes_dev"]
     J, s = plan.geometry.frame_count(), cfg.s
@@ -345,6 +360,109 @@ def main():
             v, kind, cores, sample, _ = run_reference(cfg, 3, 1)
             line["cpu_baseline"] = {"value": v, "unit": base["unit"], "cores": cores, "kind": kind, "sample": sample}
         except Exception as e:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_blind(args, cfg, base, rank, world, local, dist):
+    """Blind OD²BP (config 3): frames*iterations/s of BlindSolver iterations
+    (blind.cpp:194-296: 3 FFTs per frame, probe consensus, u-update)."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2011_00162_b200 as P
+    from paper_2011_00162_b200 import _lib as L, sim
+
+    inp = sim.make_inputs(cfg, device=True)
+    plan, amp = inp["plan"], inp["amplitudes_dev"]
+    J, s = plan.geometry.frame_count(), cfg.s
+    w0 = inp.get("w0")
+    nccl_id = None
+    if world > 1:
+        buf = C.create_string_buffer(128)
+        if rank == 0:
+            L.check(L.lib().pdd_nccl_unique_id(buf))
+        nccl_id = bcast_obj(dist, bytes(buf.raw) if rank == 0 else None, rank)
+    bcfg = P.BlindConfig(max_iters=max(cfg.iterations, args.steps + args.warmup + 8), tol_rf=1e-300, **cfg.solver)
+    solver = P.BlindSolver(plan, None, bcfg, amplitudes=amp, dtype=cfg.dtype, device=local, rank=rank, world=world,
+                           nccl_id=nccl_id)
+    L.check(L.lib().pdd_blind_init_state(solver._h, L.ptr(None if w0 is None else L.c128(w0))))
+
+    def timed(n):
+        ms = C.c_double()
+        L.check(L.lib().pdd_blind_iterate_timed(solver._h, C.c_int32(n), C.byref(ms)))
+        return ms.value
+
+    timed(args.warmup)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms_total = timed(args.steps)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = allmax(dist, ms_total)
+    prof = (C.c_double * 3)()
+    L.check(L.lib().pdd_blind_profile(solver._h, C.c_int32(3), prof))
+    ms_frame, ms_gather, ms_iter = prof[0], prof[1], prof[2]
+    p = 4 if cfg.dtype == "f32" else 8
+    j_local = sum(solver.sub_frames)
+    k1_bytes = 5 * p * j_local * s * s
+    iter_bytes = 5 * p * J * s * s + 5 * p * sum(r.area() for r in plan.subdomains)
+    peak, peak_kind = hbm_peak()
+    k1_gbs = k1_bytes / (ms_frame / 1e3) / 1e9
+    line = dict(base, impl="ours", value=J * args.steps / (ms_total / 1e3), ms_per_step=ms_total / args.steps,
+                scaling="strong", dtype=cfg.dtype,
+                config={"workload": f"BASELINE config {args.config} ({cfg.name}, blind): {cfg.N}^2 object, {s}^2 "
+                                    f"probe, step {cfg.step}, {J} frames, plan {cfg.plan}, disk w0 r="
+                                    f"{cfg.init_disk_radius}, {cfg.dtype}",
+                        "frames": J, "parallelism": f"subdomains over {world} GPU(s)",
+                        "l2": "working set ~0.8 GB > L2 (no flush needed)"},
+                roofline={"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
+                          "traffic": None, "kernel": "frame_kernel BLIND (K1)", "kernel_ms": ms_frame,
+                          "algorithmic_bytes_per_launch": k1_bytes, "peak_kind": peak_kind},
+                iter_roofline={"bytes_per_iter": iter_bytes,
+                               "achieved_gbs": iter_bytes / (ms_total / args.steps / 1e3) / 1e9,
+                               "frac": iter_bytes / (ms_total / args.steps / 1e3) / 1e9 / peak,
+                               "gather_ms": ms_gather, "profiled_iter_ms": ms_iter},
+                clocks=clk.summary(), gpu_launches=solver.launches_per_iteration() * args.steps)
+    del solver
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        host = torch.empty(amp.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(amp)
+        amp_np = host.numpy()
+        del amp
+        torch.cuda.empty_cache()
+        if dist:
+            dist.barrier()
+        ecfg = P.BlindConfig(max_iters=cfg.iterations, tol_rf=1e-300, **cfg.solver)
+        t0 = time.perf_counter()
+        s2 = P.BlindSolver(plan, None, ecfg, amplitudes=amp_np, dtype=cfg.dtype, device=local, rank=rank,
+                           world=world, nccl_id=nccl_id)
+        res = s2.run(w0=w0)
+        torch.cuda.synchronize()
+        t_e2e = allmax(dist, time.perf_counter() - t0)
+        g = plan.geometry
+        n_local = sum(h * w for h, w in s2.sub_hw)
+        line["e2e"] = {"value": J * res.iterations / t_e2e, "unit": base["unit"],
+                       "h2d_bytes_per_step": j_local * s * s * 4 + (0 if w0 is None else w0.size * 16),
+                       "d2h_bytes_per_step": n_local * 16 + (g.image_height * g.image_width * 16 if world == 1 else 0)
+                       + 3 * s * s * 16 + res.iterations * 24,
+                       "iterations_per_step": res.iterations,
+                       "timer": "host wall clock around synchronous C-ABI calls (create+upload, run, download)"}
+        del s2
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, kind, cores, sample, _ = run_reference(cfg, 2, 1)
+            line["cpu_baseline"] = {"value": v, "unit": base["unit"], "cores": cores, "kind": kind, "sample": sample}
+        except Exception as e:
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)

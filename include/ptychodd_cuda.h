@@ -211,6 +211,10 @@ PDD_API int pdd_blind_step(pdd_blind* h, int32_t store_z);
 /* run() from the current state; records [max_iters][3] */
 PDD_API int pdd_blind_run(pdd_blind* h, int64_t* iterations, double* records, int64_t* diverged_at);
 PDD_API int pdd_blind_iterate(pdd_blind* h, int32_t n);
+/* device time of exactly n iterations (CUDA events on the solver stream) */
+PDD_API int pdd_blind_iterate_timed(pdd_blind* h, int32_t n, double* ms);
+/* n eager iterations: ms[3] = {BLIND frame kernel, u-gather, whole iteration} averages */
+PDD_API int pdd_blind_profile(pdd_blind* h, int32_t n, double* ms);
 /* w, w_copies [D_local][s][s], delta [D_local][s][s], then as nonblind */
 PDD_API int pdd_blind_get_state(pdd_blind* h, double* w, double* w_copies, double* delta, double* u, double* z,
                         double* gamma, double* v, double* lambda, int64_t* iteration);

@@ -365,7 +365,7 @@ class Blind final : public BlindGpu {
     z_valid_ = store_z;
   }
 
-  std::vector<double> drive(int max_total, bool poll) {
+  std::vector<double> drive(int max_total, bool poll, bool tail = true) {
     ensure_graphs();
     constexpr int kPoll = 8;
     cudaStream_t s = R.st();
@@ -398,8 +398,10 @@ class Blind final : public BlindGpu {
     }
     for (auto e : ev) cudaEventDestroy(e);
     iter_ = R.read_ctl().iter;
-    tail_.launch(s);
-    PDD_CUDA(cudaStreamSynchronize(s));
+    if (tail) {  // R-factor of the final iterate
+      tail_.launch(s);
+      PDD_CUDA(cudaStreamSynchronize(s));
+    }
     return ms;
   }
 
@@ -433,6 +435,59 @@ class Blind final : public BlindGpu {
     refresh_wd();
     R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
     drive(n, false);
+    z_valid_ = false;
+  }
+
+  double iterate_timed(int n) override {  // exactly n iterations, CUDA events on the solver stream
+    if (n <= 0) return 0.0;
+    refresh_wd();
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
+    ensure_graphs();
+    cudaEvent_t e0, e1;
+    PDD_CUDA(cudaEventCreate(&e0));
+    PDD_CUDA(cudaEventCreate(&e1));
+    PDD_CUDA(cudaEventRecord(e0, R.st()));
+    drive(n, false, false);
+    PDD_CUDA(cudaEventRecord(e1, R.st()));
+    PDD_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PDD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    z_valid_ = false;
+    return ms;
+  }
+
+  // n eager iterations: ms[0] frame kernel (BLIND mode), ms[1] u-gather, ms[2] whole iteration.
+  void profile(int n, double* out) override {
+    cudaEvent_t ev[4], e_start, e_end;
+    for (auto& e : ev) PDD_CUDA(cudaEventCreate(&e));
+    PDD_CUDA(cudaEventCreate(&e_start));
+    PDD_CUDA(cudaEventCreate(&e_end));
+    refresh_wd();
+    R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + n, 2, cfg_.tol_rf, cfg_.tol_re);
+    double fr = 0.0, ga = 0.0;
+    PDD_CUDA(cudaEventRecord(e_start, R.st()));
+    for (int i = 0; i < n; ++i) {
+      enqueue_iteration(static_cast<int>(iter_ & 1), false, ev);
+      PDD_CUDA(cudaEventSynchronize(ev[3]));
+      float a = 0.f, b = 0.f;
+      PDD_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+      PDD_CUDA(cudaEventElapsedTime(&b, ev[2], ev[3]));
+      fr += a;
+      ga += b;
+      ++iter_;
+    }
+    PDD_CUDA(cudaEventRecord(e_end, R.st()));
+    PDD_CUDA(cudaEventSynchronize(e_end));
+    float tot = 0.f;
+    PDD_CUDA(cudaEventElapsedTime(&tot, e_start, e_end));
+    out[0] = fr / n;
+    out[1] = ga / n;
+    out[2] = tot / n;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e_start);
+    cudaEventDestroy(e_end);
     z_valid_ = false;
   }
 

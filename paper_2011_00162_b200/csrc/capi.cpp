@@ -653,6 +653,12 @@ int pdd_blind_run(pdd_blind* h, int64_t* iterations, double* records, int64_t* d
   NB_CALL(h, records_out(h->s->run(), iterations, records, diverged_at));
 }
 int pdd_blind_iterate(pdd_blind* h, int32_t n) { NB_CALL(h, h->s->iterate(n)); }
+int pdd_blind_iterate_timed(pdd_blind* h, int32_t n, double* ms) {
+  NB_CALL(h, need(ms, "ms"); *ms = h->s->iterate_timed(n));
+}
+int pdd_blind_profile(pdd_blind* h, int32_t n, double* ms) {
+  NB_CALL(h, need(ms, "ms"); if (n < 1) throw pdd::InvalidArgument("profile: n >= 1"); h->s->profile(n, ms));
+}
 int pdd_blind_get_state(pdd_blind* h, double* w, double* w_copies, double* delta, double* u, double* z, double* gamma,
                         double* v, double* lambda, int64_t* iteration) {
   NB_CALL(h, h->s->get_state(w, w_copies, delta, u, z, gamma, v, lambda, iteration));

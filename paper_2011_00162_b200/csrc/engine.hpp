@@ -121,6 +121,8 @@ class BlindGpu {
   virtual void step(bool store_z) = 0;
   virtual RunRecords run() = 0;
   virtual void iterate(int n) = 0;
+  virtual double iterate_timed(int n) = 0;          // device ms of exactly n iterations
+  virtual void profile(int n, double* ms) = 0;      // {frame kernel, u-gather, iteration} averages
   virtual void get_state(double* w, double* w_copies, double* delta, double* u, double* z, double* gamma, double* v,
                          double* lam, int64_t* iteration) = 0;
   virtual void set_state(const double* w, const double* w_copies, const double* delta, const double* u,

@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
   double diff = 0.0, nrm = 0.0;
   const int64_t base = a.sub_off[sub];
   constexpr bool update = MODE == kGatherNonblind || MODE == kGatherBlind;
+  const cx<T>* u_in = a.u_in ? a.u_in : a.u;
+  const cx<T>* lam_in = a.lam_in ? a.lam_in : a.lam;
   int pb = 0, pe = 0;
   if constexpr (update) {
     pb = a.sub_pbeg[sub];
@@ -347,9 +349,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
           const PairSide p = a.ps[q];
           if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
           const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
-          num += (a.v[p.v_off + o] - a.lam[p.lam_off + o]) * a.r;
+          num += (a.v[p.v_off + o] - lam_in[p.lam_off + o]) * a.r;
         }
-        const cx<T> uo = a.u[pi];
+        const cx<T> uo = u_in[pi];
         cx<T> un;
         if constexpr (MODE == kGatherNonblind) {
           const T d = a.denom[pi];
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
           const PairSide p = a.ps[q];
           if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
           const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
-          a.lam[p.lam_off + o] += un - a.v[p.v_off + o];
+          a.lam[p.lam_off + o] = lam_in[p.lam_off + o] + (un - a.v[p.v_off + o]);
         }
         a.u[pi] = un;
         const double dx = static_cast<double>(un.x) - static_cast<double>(uo.x);

@@ -44,13 +44,15 @@ struct GatherArgs {
   const int64_t* sub_off = nullptr;     // [nsub] offset into image buffers
   const int32_t* sub_h = nullptr;
   const int32_t* sub_w = nullptr;
-  cx<T>* u = nullptr;
+  cx<T>* u = nullptr;                   // updates: output image (u^{n+1})
+  const cx<T>* u_in = nullptr;          // updates: u^n when not in place (nullptr: u)
   const T* denom = nullptr;             // nonblind: eta*rho + r*npairs (< 0: pinned)
   const T* rpen = nullptr;              // blind: r*npairs (< 0: pinned)
   const int32_t* sub_pbeg = nullptr;    // CSR over PairSide per subdomain (ascending p)
   const PairSide* ps = nullptr;
   const cx<T>* v = nullptr;
-  cx<T>* lam = nullptr;
+  cx<T>* lam = nullptr;                 // updates: Lambda^{n+1}
+  const cx<T>* lam_in = nullptr;        // Lambda^n when not in place (nullptr: lam)
   T eta = T(0), r = T(0), gamma = T(0);
   cx<T>* out = nullptr;                 // adjoint output (image layout)
   double* dens_out = nullptr;           // density output (image layout)

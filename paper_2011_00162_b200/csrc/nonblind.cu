@@ -46,9 +46,11 @@ class Nonblind final : public NonblindGpu {
     gamma_[0].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
     gamma_[1].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
     bp_.alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
-    u_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.img_elems, 1));
-    v_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.v_elems, 1));
-    lam_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.lam_elems, 1));
+    for (int p = 0; p < 2; ++p) {  // iterate ping-pong (state of iteration n in [n & 1])
+      u_[p].alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.img_elems, 1));
+      v_[p].alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.v_elems, 1));
+      lam_[p].alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.lam_elems, 1));
+    }
     s_.alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.s_elems, 1));
     SetupTimer tm;
     build_denominators();
@@ -108,10 +110,10 @@ class Nonblind final : public NonblindGpu {
 
   void init_state() override {  // solver.cpp:96-116
     cudaStream_t s = R.st();
-    PDD_CUDA(launch_fill<T>(u_.as<cx<T>>(), R.L.img_elems, cx<T>{T(1), T(0)}, s));
+    PDD_CUDA(launch_fill<T>(U(0), R.L.img_elems, cx<T>{T(1), T(0)}, s));
     PDD_CUDA(cudaMemsetAsync(gamma_[0].get(), 0, gamma_[0].bytes(), s));
-    PDD_CUDA(cudaMemsetAsync(lam_.get(), 0, lam_.bytes(), s));
-    R.consensus(u_.as<cx<T>>(), lam_.as<cx<T>>(), s_.as<cx<T>>(), v_.as<cx<T>>(), nullptr);
+    PDD_CUDA(cudaMemsetAsync(lam_[0].get(), 0, lam_[0].bytes(), s));
+    R.consensus(U(0), LAM(0), s_.as<cx<T>>(), V(0), nullptr);
     iter_ = 0;
     z_valid_ = false;
     if (z_.bytes()) {  // z^0 = A u^0
@@ -121,10 +123,14 @@ class Nonblind final : public NonblindGpu {
     PDD_CUDA(cudaStreamSynchronize(s));
   }
 
+  cx<T>* U(int64_t p) const { return u_[p & 1].template as<cx<T>>(); }
+  cx<T>* V(int64_t p) const { return v_[p & 1].template as<cx<T>>(); }
+  cx<T>* LAM(int64_t p) const { return lam_[p & 1].template as<cx<T>>(); }
+
   void forward_into(cx<T>* out, double* rf_part = nullptr) {
     FrameArgs<T> a = R.frame_args();
     a.probe = probe_.as<cx<T>>();
-    a.img = u_.as<cx<T>>();
+    a.img = U(iter_);
     a.frames_out = out;
     a.rf_part = rf_part;
     PDD_CUDA(launch_frame<T>(kFwd, R.S, a, R.st()));
@@ -138,7 +144,7 @@ class Nonblind final : public NonblindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[0], s));
     FrameArgs<T> a = R.frame_args();
     a.probe = probe_.as<cx<T>>();
-    a.img = u_.as<cx<T>>();
+    a.img = U(parity);
     a.gamma_in = gamma_[parity].as<cx<T>>();
     a.gamma_out = gamma_[1 - parity].as<cx<T>>();
     a.z_out = store_z ? z_.as<cx<T>>() : nullptr;
@@ -152,13 +158,16 @@ class Nonblind final : public NonblindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
     R.reduce_rf(true);
     PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
-    R.consensus(u_.as<cx<T>>(), lam_.as<cx<T>>(), s_.as<cx<T>>(), v_.as<cx<T>>(), R.skipB());
+    // v^{n+1} from u^n, Lambda^n (solver.cpp:141-151) into the outgoing parity
+    R.consensus(U(parity), LAM(parity), s_.as<cx<T>>(), V(1 - parity), R.skipB());
     GatherArgs<T> g = R.gather_args(kGatherNonblind);
     g.bp = bp_.as<cx<T>>();
-    g.u = u_.as<cx<T>>();
+    g.u_in = U(parity);
+    g.u = U(1 - parity);
     g.denom = denom_.as<T>();
-    g.v = v_.as<cx<T>>();
-    g.lam = lam_.as<cx<T>>();
+    g.v = V(1 - parity);
+    g.lam_in = LAM(parity);
+    g.lam = LAM(1 - parity);
     g.eta = static_cast<T>(cfg_.eta);
     g.r = static_cast<T>(cfg_.r);
     g.re_part = R.re_part.template as<double>();
@@ -176,10 +185,9 @@ class Nonblind final : public NonblindGpu {
     PDD_CUDA(launch_gate(R.ctlp(), s));
     FrameArgs<T> a = R.frame_args();
     a.probe = probe_.as<cx<T>>();
-    a.img = u_.as<cx<T>>();
+    a.img = U(parity);
     a.rf_part = R.rf_part.template as<double>();
     a.stop_flag = R.skipA();
-    (void)parity;
     PDD_CUDA(launch_frame<T>(kFwd, R.S, a, s));
     R.reduce_rf(true);
     PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
@@ -272,8 +280,8 @@ class Nonblind final : public NonblindGpu {
     PDD_CUDA(launch_lagrangian_frames<T>(bp_.as<cx<T>>(), z_.as<cx<T>>(), gamma_[iter_ & 1].as<cx<T>>(),
                                          R.amp.template as<T>(), R.L.nfr, R.SS(), cfg_.epsilon, cfg_.eta,
                                          lag_fr_.as<double>(), s));
-    PDD_CUDA(launch_lagrangian_pairs<T>(R.pgeom.template as<PairGeom>(), np, u_.as<cx<T>>(), v_.as<cx<T>>(),
-                                        lam_.as<cx<T>>(), cfg_.r, lag_pr_.as<double>(), s));
+    PDD_CUDA(launch_lagrangian_pairs<T>(R.pgeom.template as<PairGeom>(), np, U(iter_), V(iter_), LAM(iter_), cfg_.r,
+                                        lag_pr_.as<double>(), s));
     const size_t P = plan_.overlaps.size();
     double* glob = lag_glob_.as<double>();  // [D] frame terms, then [P][2] overlap terms
     PDD_CUDA(cudaMemsetAsync(glob, 0, sizeof(double) * (R.D + 2 * P), s));
@@ -434,7 +442,7 @@ class Nonblind final : public NonblindGpu {
   void get_state(double* u, double* z, double* gamma, double* v, double* lam, int64_t* iteration) override {
     cudaStream_t s = R.st();
     const int64_t nf = R.L.nfr * R.SS();
-    if (u) download_c128<T>(u_.get(), R.L.img_elems, u, s);
+    if (u) download_c128<T>(U(iter_), R.L.img_elems, u, s);
     if (gamma) download_c128<T>(gamma_[iter_ & 1].get(), nf, gamma, s);
     if (z) {
       if (!z_valid_) {
@@ -444,8 +452,8 @@ class Nonblind final : public NonblindGpu {
         download_c128<T>(z_.get(), nf, z, s);
       }
     }
-    if (v) download_c128<T>(v_.get(), R.L.v_elems, v, s);
-    if (lam) download_c128<T>(lam_.get(), R.L.lam_elems, lam, s);
+    if (v) download_c128<T>(V(iter_), R.L.v_elems, v, s);
+    if (lam) download_c128<T>(LAM(iter_), R.L.lam_elems, lam, s);
     if (iteration) *iteration = iter_;
   }
 
@@ -454,15 +462,15 @@ class Nonblind final : public NonblindGpu {
     cudaStream_t s = R.st();
     const int64_t nf = R.L.nfr * R.SS();
     iter_ = iteration;
-    if (u) upload_cx<T>(u_.get(), u, R.L.img_elems, s);
+    if (u) upload_cx<T>(U(iter_), u, R.L.img_elems, s);
     if (gamma) upload_cx<T>(gamma_[iter_ & 1].get(), gamma, nf, s);
     if (z) {
       ensure_z();
       upload_cx<T>(z_.get(), z, nf, s);
       z_valid_ = true;
     }
-    if (v) upload_cx<T>(v_.get(), v, R.L.v_elems, s);
-    if (lam) upload_cx<T>(lam_.get(), lam, R.L.lam_elems, s);
+    if (v) upload_cx<T>(V(iter_), v, R.L.v_elems, s);
+    if (lam) upload_cx<T>(LAM(iter_), lam, R.L.lam_elems, s);
   }
 
   void forward_frames(double* au) override {
@@ -470,7 +478,7 @@ class Nonblind final : public NonblindGpu {
     download_c128<T>(bp_.get(), R.L.nfr * R.SS(), au, R.st());
   }
 
-  void merged(double* out) override { R.merge_to_host(plan_, u_.as<cx<T>>(), out); }
+  void merged(double* out) override { R.merge_to_host(plan_, U(iter_), out); }
   void sync() override { R.stream.sync(); }
   int64_t kernel_launches_per_iteration() const override { return 10; }
 
@@ -479,7 +487,7 @@ class Nonblind final : public NonblindGpu {
   NonblindConfig cfg_;
   RankData<T> R;
   StateLayout layout_;
-  DevMem probe_, probe64_, gamma_[2], bp_, u_, v_, lam_, s_, denom_, z_;
+  DevMem probe_, probe64_, gamma_[2], bp_, u_[2], v_[2], lam_[2], s_, denom_, z_;
   DevMem lag_fr_, lag_pr_, lag_glob_;
   std::vector<double> last_lag_;
   Graph full_[2], tail_[2];

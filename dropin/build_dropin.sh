@@ -13,7 +13,8 @@
 #   - paper_2011_00162_b200/libptychodd_cuda.so.
 # The test framework header is dropin/doctest.h (doctest is not in the image).
 # Also the reference's acceptance program (proj/tests/acceptance.cpp, the
-# paper's criteria 1-6) linked the same way.
+# paper's criteria 1-6) and its pybind module (proj/python/bindings.cpp ->
+# _ptychodd) linked the same way.
 # Output: dropin/_build/ptychodd_dropin_{tests,acceptance} (git-ignored; they
 # travel to the GPU box with the snapshot).
 set -euo pipefail
@@ -48,5 +49,21 @@ link "$out/ptychodd_dropin_tests" "${objs[@]}"
 lib_objs=()
 for o in "${objs[@]}"; do case "$o" in */test_*.o) ;; *) lib_objs+=("$o") ;; esac; done
 link "$out/ptychodd_dropin_acceptance" "${lib_objs[@]}" "$out/acceptance.o"
+# the reference's pybind front-end (proj/python/bindings.cpp, unmodified): the
+# Python reconstruct / reconstruct_blind entry points routed to the GPU library
+pyinc="$(python3 -c 'import sysconfig; print(sysconfig.get_paths()["include"])')"
+pybind="$(python3 -c 'import pybind11; print(pybind11.get_include())')"
+ext="$(python3 -c 'import sysconfig; print(sysconfig.get_config_var("EXT_SUFFIX"))')"
+PYCXX="g++ -std=c++20 -O2 -DNDEBUG -fPIC -fvisibility=hidden -I$ref/include -I$here -I$repo/include -I$pyinc -I$pybind"
+pyobjs=()
+for s in field scan ddplan simulate metrics; do
+  $PYCXX -c "$ref/src/$s.cpp" -o "$out/py_ref_$s.o" & pyobjs+=("$out/py_ref_$s.o")
+done
+$PYCXX -c "$here/ptychodd_solver_cuda.cpp" -o "$out/py_solver.o" & pyobjs+=("$out/py_solver.o")
+$PYCXX -c "$here/ptychodd_ops_cuda.cpp" -o "$out/py_ops.o" & pyobjs+=("$out/py_ops.o")
+$PYCXX -c "$ref/python/bindings.cpp" -o "$out/py_bindings.o" & pyobjs+=("$out/py_bindings.o")
+wait
+g++ -shared -o "$out/_ptychodd$ext" "${pyobjs[@]}" -L"$lib" -lptychodd_cuda \
+  -Wl,-rpath,'$ORIGIN/../../paper_2011_00162_b200' -lpthread
 rm -f "$out"/*.o
-echo "built $out/ptychodd_dropin_tests $out/ptychodd_dropin_acceptance"
+echo "built $out/ptychodd_dropin_tests $out/ptychodd_dropin_acceptance $out/_ptychodd$ext"

@@ -50,3 +50,51 @@ def test_reference_acceptance_criteria_on_the_gpu_library():
         assert re.search(rf"^PASS criterion {c}:", r.stdout, re.M), r.stdout
     m = re.search(r"D=10/D=1 = ([0-9.]+) \(<=1.20\)", r.stdout)
     assert m and float(m.group(1)) <= 1.20, r.stdout
+
+
+BUILD = os.path.join(ROOT, "dropin", "_build")
+HAVE_PY = os.path.isdir(BUILD) and any(n.startswith("_ptychodd") and n.endswith(".so") for n in os.listdir(BUILD))
+
+
+def _pt():
+    import sys
+
+    if BUILD not in sys.path:
+        sys.path.insert(0, BUILD)
+    import _ptychodd
+
+    return _ptychodd
+
+
+def _toy(pt, size=48, probe_side=16, step=8, seed=11):
+    g = pt.make_raster_scan(size, size, probe_side, step)
+    border = probe_side // 2
+    mag, ph = pt.make_test_images(size, size, border, seed)
+    sample = pt.make_sample(mag, ph, g)
+    probe = pt.make_zone_plate_probe(probe_side)
+    frames = pt.simulate_frames(probe, sample, g)
+    pin = pt.vacuum_border_mask(size, size, border)
+    return g, sample, probe, frames, pin
+
+
+@pytest.mark.skipif(not HAVE_PY, reason="drop-in pybind module not built (needs /root/reference)")
+def test_reference_pybind_frontend_routes_to_the_gpu_library():
+    """proj/python/bindings.cpp (the reference's Python front-end, unmodified)
+    compiled against the drop-in: reconstruct / reconstruct_blind run the
+    solvers of libptychodd_cuda.so."""
+    import numpy as np
+
+    pt = _pt()
+    g, sample, probe, frames, pin = _toy(pt)
+    fw = pt.forward(probe, sample, g)  # GPU forward operator
+    for j, z in enumerate(fw):
+        np.testing.assert_allclose(np.abs(z) ** 2, frames[j], rtol=1e-10, atol=1e-8)
+    res = pt.reconstruct(frames, g, probe, subdomains=2, r=3.0e2, max_iters=200, pin=pin)
+    assert res["merged"].shape == (48, 48) and res["rf"] < 1e-3
+    assert pt.snr_db(res["merged"], sample) > 30.0
+    blind = pt.reconstruct_blind(frames, g, subdomains=2, r=1.0e3, max_iters=40, pin=pin)
+    assert blind["probe"].shape == (16, 16) and np.isfinite(blind["rf"])
+    assert np.all(blind["probe_fourier"][blind["support_mask"] == 0.0] == 0.0)
+    # the library behind the module is the in-tree CUDA library
+    with open(f"/proc/{os.getpid()}/maps") as fh:
+        assert "libptychodd_cuda.so" in fh.read()

@@ -109,6 +109,7 @@ struct RankData {
   DevMem pin_dev;  // uint8 per local image pixel
   double l1 = 0.0;
   int D = 0;
+  bool rows_al16 = false;  // every window row 16-byte aligned in the image buffers
   int rec_cap = 0;
 
   cudaStream_t st() const { return stream.get(); }
@@ -137,6 +138,9 @@ struct RankData {
     cudaStream_t s = st();
     tw = upload(twiddles<T>(S), s);
     fr_off = upload(L.fr_off, s);
+    rows_al16 = (sizeof(cx<T>) >= 16) ||
+                (std::all_of(L.fr_off.begin(), L.fr_off.end(), [](int64_t o) { return o % 2 == 0; }) &&
+                 std::all_of(L.fr_pitch.begin(), L.fr_pitch.end(), [](int32_t p) { return p % 2 == 0; }));
     fr_pitch = upload(L.fr_pitch, s);
     fr_r = upload(L.fr_r, s);
     fr_c = upload(L.fr_c, s);
@@ -274,6 +278,7 @@ struct RankData {
     a.pitch = fr_pitch.as<int32_t>();
     a.amp = amp.as<T>();
     a.scale = static_cast<T>(1.0 / static_cast<double>(S));
+    a.rows_al16 = rows_al16 ? 1 : 0;
     return a;
   }
 

@@ -38,6 +38,7 @@ struct StreamShape {
   static constexpr int CG = NT / GC;         // columns per group
   static constexpr int NG = S / CG;          // column groups
   static constexpr int P = S + GR;           // smem pitch (bank-conflict-free with the rotation swizzle)
+  static constexpr int RW = 32 / GR;         // rows per warp in the row phases
   static_assert(RR >= GR && RR % GR == 0, "row split");
   static_assert(RC >= GC && RC % GC == 0, "column split");
   static_assert(S % RPB == 0 && S % CG == 0 && CG >= 32, "grouping");
@@ -118,6 +119,32 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
   };
 
+  // Patch rows by bulk TMA: in the inverse row phase each warp's own rows of
+  // buf fall free; 4 lanes then copy the next frame's patch rows for the same
+  // warp and row batch into them (1 KB each, completion on a per-(warp, batch)
+  // mbarrier), so the forward row phase reads them from shared memory instead
+  // of waiting on HBM.  Needs 16-byte aligned rows (even window offsets and
+  // pitches; checked on the host).
+  constexpr int NW = NT / 32;
+  __shared__ __align__(8) uint64_t s_rowbar[NW * NRB];
+  const bool tma_rows = !FWD && a.rows_al16 != 0 && sizeof(cx<T>) * S % 16 == 0;
+  if (tma_rows) {
+    if (t < NW * NRB) mbar_init(s_rowbar + t, 1);
+    mbar_init_fence();
+    __syncthreads();
+  }
+  auto issue_rows = [&](int ff, int rb) {  // whole warp; rows rb*RPB + RW*warp + [0, RW)
+    const int lane = t & 31;
+    uint64_t* bar = s_rowbar + rb * NW + warp;
+    if (lane == 0) mbar_arrive_expect_tx(bar, SH::RW * S * sizeof(cx<T>));
+    __syncwarp();
+    if (lane < SH::RW) {
+      const int y = rb * RPB + SH::RW * warp + lane;
+      bulk_g2s(buf + y * P, a.img + a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff], S * sizeof(cx<T>), bar);
+    }
+  };
+  uint32_t row_phase = 0;  // parity of the frames consumed so far
+
   const T scale = TMEMP ? T(1) : a.scale;  // TMEM probe carries the 1/S
   const T inv1pl = T(1) / (T(1) + a.lam);
   const int cx_ = t % CG, gc = t / CG;  // column-phase coordinates
@@ -139,6 +166,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
   };
   prefetch(blockIdx.x, 0);
+  if (tma_rows && blockIdx.x < a.nframes)
+#pragma unroll 1
+    for (int rb = 0; rb < NRB; ++rb) issue_rows(blockIdx.x, rb);
 
 #ifdef PDD_PHASE_TIMING
   unsigned long long tph[4] = {0, 0, 0, 0};
@@ -161,9 +191,16 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
       cx<T> v[RR], pv[RR];
-      const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
+      if (tma_rows) {
+        mbar_wait(s_rowbar + rb * NW + warp, row_phase);
 #pragma unroll
-      for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
+        for (int m = 0; m < RR; ++m) v[m] = buf[y * P + g + GR * m];
+        __syncwarp();  // all lanes hold their row elements before the row is overwritten
+      } else {
+        const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
+#pragma unroll
+        for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
+      }
       probe_row(rb, y, g, pv);
 #pragma unroll
       for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
@@ -305,6 +342,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         const cx<T> b = buf[y * P + k * GR + ((g + k) & (GR - 1))];
         v[k] = (k == 0) ? b : mul_conj(b, twr[k * GR + g]);
       }
+      if (tma_rows && f + static_cast<int>(gridDim.x) < a.nframes) {
+        __syncwarp();             // this warp's rows are consumed
+        fence_proxy_async_smem();  // ... before the async proxy overwrites them
+        issue_rows(f + gridDim.x, rb);
+      }
       dft<RR, true>(v);
       cx<T>* dst = a.bp_out + fbase + y * S + g;
 #pragma unroll
@@ -312,6 +354,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
 
     PDD_TICK(2);
+    row_phase ^= 1u;
     // per-frame R-factor partial (deterministic tree)
     double rf = static_cast<double>(rf_acc);
     if (a.rf_part) {

@@ -199,7 +199,7 @@ __device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b)
 // so the NROW x unroll predicated loads of one trip are all in flight before
 // the first add waits on one of them.
 template <typename T, int NROW, int VEC, int MODE>
-__global__ void __launch_bounds__(256) gather_kernel(const GatherArgs<T> a) {
+__global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGatherAdjoint) ? 4 : 1) gather_kernel(const GatherArgs<T> a) {
   constexpr int kMeta = 256;  // covering frames staged in shared memory per chunk
   __shared__ double sm[16];
   __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta];

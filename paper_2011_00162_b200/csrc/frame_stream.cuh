@@ -18,7 +18,7 @@
 // walk frames with a grid stride.  Loops over row batches and column groups
 // are not unrolled, which keeps the SASS inside the instruction cache (the
 // fully unrolled engine spent a quarter of its stall samples on
-// no_instructions, profiles/r1_frame_kernel_c4.txt).
+// no_instructions in its ncu capture).
 #pragma once
 
 #include <type_traits>

@@ -88,9 +88,11 @@ def test_one_sweep_matches_oracle(dtype, tol, D, grid):
 
 
 @pytest.mark.parametrize("N,s,step,grid", [(256, 64, 16, None), (512, 128, 32, None), (512, 128, 32, (2, 2)),
-                                           (384, 64, 16, (2, 3))])
+                                           (384, 64, 16, (2, 3)), (285, 64, 17, None), (350, 128, 37, None)])
 def test_streamed_sweep_large_frames_matches_oracle(N, s, step, grid):
-    """s = 64 / 128 float32 sweeps run the streamed kernel (frame_stream.cuh)."""
+    """s = 64 / 128 float32 sweeps run the streamed kernel (frame_stream.cuh).
+    Odd steps put window rows at 8-byte but not 16-byte boundaries: the patch
+    rows then come by plain loads instead of bulk TMA."""
     probe, f, oplan, plan = small_problem(N=N, s=s, step=step, D=2, peak=1e4, grid=grid)
     f = fp32_intensity(f)
     gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f32")

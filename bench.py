@@ -425,7 +425,7 @@ def bench_blind(args, cfg, base, rank, world, local, dist):
                         "frames": J, "parallelism": f"subdomains over {world} GPU(s)",
                         "l2": "working set ~0.8 GB > L2 (no flush needed)"},
                 roofline={"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
-                          "traffic": None, "kernel": "frame_kernel BLIND (K1)", "kernel_ms": ms_frame,
+                          "traffic": None, "kernel": "BLIND frame pass (K1: R-factor forward + streamed sweep)", "kernel_ms": ms_frame,
                           "algorithmic_bytes_per_launch": k1_bytes, "peak_kind": peak_kind},
                 iter_roofline={"bytes_per_iter": iter_bytes,
                                "achieved_gbs": iter_bytes / (ms_total / args.steps / 1e3) / 1e9,

@@ -552,7 +552,10 @@ class Blind final : public BlindGpu {
 
   void merged(double* out) override { R.merge_to_host(plan_, u_.as<cx<T>>(), out); }
   void sync() override { R.stream.sync(); }
-  int64_t kernel_launches_per_iteration() const override { return 17; }
+  // float32 s = 64: the BLIND frame pass is two streamed launches (kernels.cu)
+  int64_t kernel_launches_per_iteration() const override {
+    return std::is_same_v<T, float> && R.S == 64 ? 18 : 17;
+  }
 
  private:
   Plan plan_;

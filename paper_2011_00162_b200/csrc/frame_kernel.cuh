@@ -48,6 +48,7 @@ struct FrameArgs {
   T scale = T(1);                     // 1/S (unitary normalisation per transform)
   unsigned long long* phase_cycles = nullptr;  // PDD_PHASE_TIMING builds: per-phase SM cycles
   int rows_al16 = 0;                  // every window row starts 16-byte aligned (streamed kernel: TMA rows)
+  int bp_raw = 0;                     // SWEEP: bp_out = IFFT(.) without conj(probe) (the blind q_j)
 };
 
 // ST-AGM per-pixel prox, stagm.cpp:45-73.  amp = sqrt(b).  The fast form is

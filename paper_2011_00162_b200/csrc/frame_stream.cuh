@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   }
   __syncthreads();
   // this thread's probe values for row batch rb, from TMEM or global memory
-  auto probe_row = [&](int rb, int y, int g, cx<T>* pv) {
+  auto probe_row = [&](int ff, int rb, int y, int g, cx<T>* pv) {
     if constexpr (TMEMP) {
       uint32_t raw[32];
       tmem_ld32(tmem_addr(tmem_base, warp, (warp >> 2) * ProbeTmem<SH>::PER_THREAD + 32 * rb), raw);
@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int m = 0; m < RR; ++m) pv[m] = cx<T>{__uint_as_float(raw[2 * m]), __uint_as_float(raw[2 * m + 1])};
     } else {
-      const cx<T>* pr = a.probe + y * S + g;
+      // per-frame probe tiles (blind: the subdomain's copy W_d) via probe_idx
+      const cx<T>* pr =
+          a.probe + (a.probe_idx ? static_cast<int64_t>(a.probe_idx[ff]) * S * S : int64_t(0)) + y * S + g;
 #pragma unroll
       for (int m = 0; m < RR; ++m) pv[m] = pr[GR * m];
     }
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
       }
-      probe_row(rb, y, g, pv);
+      probe_row(f, rb, y, g, pv);
 #pragma unroll
       for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
       dft<RR, false>(v);
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int rb = 0; rb < (FWD ? 0 : NRB); ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
       cx<T> v[RR], pv[RR];
-      probe_row(rb, y, g, pv);
+      probe_row(f, rb, y, g, pv);
 #pragma unroll
       for (int q = 0; q < RR / GR; ++q) {
         const int k2 = g + GR * q;
@@ -350,7 +352,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       dft<RR, true>(v);
       cx<T>* dst = a.bp_out + fbase + y * S + g;
 #pragma unroll
-      for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pv[m]);
+      if (a.bp_raw) {  // blind: q_j = IFFT(.) itself; conj(W^{n+1}) is applied in the gather
+#pragma unroll
+        for (int m = 0; m < RR; ++m) dst[GR * m] = v[m] * scale;
+      } else {
+#pragma unroll
+        for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pv[m]);
+      }
     }
 
     PDD_TICK(2);

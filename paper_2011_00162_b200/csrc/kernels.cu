@@ -84,6 +84,24 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
     using SH = typename StreamPick<T, S>::type;
     return a.fast_prox ? launch_stream<T, SH, true, true>(a, st) : launch_stream<T, SH, false, true>(a, st);
   }
+  if constexpr (MODE == kBlind && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
+    using SH = typename StreamPick<T, S>::type;
+    if constexpr (SH::MINB > 1) {  // no TMEM probe cache: per-frame probe tiles are fine
+      // BLIND = R-factor forward with the shared probe w (probe2), then the
+      // SWEEP with the subdomain copies W_d and raw q_j output
+      FrameArgs<T> rf = a;
+      rf.probe = a.probe2;
+      rf.probe_idx = nullptr;
+      rf.frames_out = nullptr;
+      rf.inten_out = nullptr;
+      cudaError_t e = a.rf_part ? launch_frame_s<T, S, kFwd>(rf, st) : cudaSuccess;
+      if (e != cudaSuccess) return e;
+      FrameArgs<T> sw = a;
+      sw.rf_part = nullptr;
+      sw.bp_raw = 1;
+      return a.fast_prox ? launch_stream<T, SH, true>(sw, st) : launch_stream<T, SH, false>(sw, st);
+    }
+  }
   using C = FrameCfg<T, S>;
   using E = Fft2<T, S, C::R>;
   constexpr int threads = E::NT * C::FPB;

@@ -65,6 +65,28 @@ def test_blind_setup_and_steps_match_oracle(dtype, tol, D, grid):
     compare(st, ost, tol * 10)
 
 
+@pytest.mark.parametrize("N,step,D,grid", [(256, 16, 2, None), (320, 16, None, (2, 2)), (250, 17, 2, None)])
+def test_streamed_blind_frames_match_oracle(N, step, D, grid):
+    """float32 s = 64: the BLIND frame pass runs as two streamed launches (the
+    R-factor forward with w, then the sweep with W_d and raw q_j output)."""
+    f, oplan, plan = blind_problem(N=N, s=64, step=step, D=D or 1, grid=grid, peak=1e4)
+    f = fp32_intensity(f)
+    cfg = dict(r=5e3)
+    gs = P.BlindSolver(plan, f, P.BlindConfig(**cfg), dtype="f32")
+    osol = O.BlindSolver(oplan, f, O.BlindConfig(**cfg))
+    st, ost = gs.init_state(), osol.init_state()
+    for _ in range(2):
+        gs.step(st)
+        osol.step(ost)
+    compare(st, ost, 1e-4)
+    res = P.BlindSolver(plan, f, P.BlindConfig(max_iters=5, tol_rf=1e-300, **cfg), dtype="f32").run()
+    _, om, oprobe, _, orec = O.BlindSolver(oplan, f, O.BlindConfig(max_iters=5, tol_rf=1e-300, **cfg)).run()
+    assert np.max(np.abs(np.array([r.rf for r in res.records]) - [r.rf for r in orec]) /
+                  np.array([r.rf for r in orec])) < 1e-3
+    assert rel_l2(res.merged, om) < 1e-3
+    assert rel_l2(res.probe, oprobe) < 1e-3
+
+
 @pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-5)])
 def test_blind_custom_initial_probe(dtype, tol):
     # config 3 style: disk initial probe, default support estimate

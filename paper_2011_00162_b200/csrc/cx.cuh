@@ -62,6 +62,91 @@ __host__ __device__ __forceinline__ T norm2(cx<T> a) {
   return a.x * a.x + a.y * a.y;
 }
 
+// ---- complex64 on sm_100 packed FP32 ---------------------------------------
+// Blackwell issues FADD2/FMUL2/FFMA2: one instruction on an (re, im) register
+// pair.  The frame kernels are issue-bound (FADD/FMUL/FFMA were 65 % of the
+// executed instructions of the streamed sweep), so complex64 add/sub is one
+// instruction and a complex multiply two (FMUL2 by the broadcast real part,
+// FFMA2 of the swapped operand by (-im, im); ptxas folds the swap and the
+// partial negation into operand modifiers).  Host code keeps the scalar forms.
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+#define PDD_F32X2 1
+namespace f32x2 {
+__device__ __forceinline__ unsigned long long pk(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ cx<float> up(unsigned long long v) {
+  cx<float> r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long add(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long sub(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("sub.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ unsigned long long fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+}  // namespace f32x2
+#endif
+
+__host__ __device__ __forceinline__ cx<float> operator+(cx<float> a, cx<float> b) {
+#ifdef PDD_F32X2
+  return f32x2::up(f32x2::add(f32x2::pk(a.x, a.y), f32x2::pk(b.x, b.y)));
+#else
+  return {a.x + b.x, a.y + b.y};
+#endif
+}
+__host__ __device__ __forceinline__ cx<float> operator-(cx<float> a, cx<float> b) {
+#ifdef PDD_F32X2
+  return f32x2::up(f32x2::sub(f32x2::pk(a.x, a.y), f32x2::pk(b.x, b.y)));
+#else
+  return {a.x - b.x, a.y - b.y};
+#endif
+}
+__host__ __device__ __forceinline__ cx<float> operator*(cx<float> a, cx<float> b) {
+#ifdef PDD_F32X2
+  const unsigned long long t = f32x2::mul(f32x2::pk(a.x, a.y), f32x2::pk(b.x, b.x));
+  return f32x2::up(f32x2::fma(f32x2::pk(a.y, a.x), f32x2::pk(-b.y, b.y), t));
+#else
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+#endif
+}
+__host__ __device__ __forceinline__ cx<float> operator*(cx<float> a, float s) {
+#ifdef PDD_F32X2
+  return f32x2::up(f32x2::mul(f32x2::pk(a.x, a.y), f32x2::pk(s, s)));
+#else
+  return {a.x * s, a.y * s};
+#endif
+}
+__host__ __device__ __forceinline__ cx<float>& operator+=(cx<float>& a, cx<float> b) {
+  a = a + b;
+  return a;
+}
+__host__ __device__ __forceinline__ cx<float> mul_conj(cx<float> a, cx<float> b) {
+#ifdef PDD_F32X2
+  const unsigned long long t = f32x2::mul(f32x2::pk(a.x, a.y), f32x2::pk(b.x, b.x));
+  return f32x2::up(f32x2::fma(f32x2::pk(a.y, a.x), f32x2::pk(b.y, -b.y), t));
+#else
+  return {a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y};
+#endif
+}
+
 // ---- compile-time loops ----------------------------------------------------
 template <int... Is, class F>
 __host__ __device__ __forceinline__ void static_for_impl(std::integer_sequence<int, Is...>, F&& f) {

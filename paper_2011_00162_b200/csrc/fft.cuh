@@ -50,7 +50,7 @@ __device__ __forceinline__ cx<T> twk(cx<T> a) {
     constexpr int m = k * (64 / N);
     constexpr T c = T(cos64(m));
     constexpr T s = INV ? T(sin64(m)) : T(-sin64(m));
-    return cx<T>{a.x * c - a.y * s, a.x * s + a.y * c};
+    return a * cx<T>{c, s};
   }
 }
 

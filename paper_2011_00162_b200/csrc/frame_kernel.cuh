@@ -100,19 +100,25 @@ __device__ __forceinline__ cx<T> stagm_prox(cx<T> y, T amp, T lam, T eps, bool f
 // Hardware rsqrt (<= 2 ulp): a Newton refinement was measured to change
 // nothing in the parity errors (Gamma's float32 error is set by cancellation
 // in y - prox(y)) while costing 5% of the frame kernel.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// The argument is clamped to FLT_MIN so the flush-to-zero rsqrt (one MUFU, no
+// denormal rescaling branch) stays finite: n2 = 0 gives |y| = 0 and the
+// reference's (m, 0) exactly; 0 < n2 < FLT_MIN (|y| < 1.1e-19, far below any
+// float32 Fourier coefficient of a frame) is treated as n2 = FLT_MIN.
 __device__ __forceinline__ cx<float> prox_fast_f32(cx<float> y, float amp, float lam, float inv1pl) {
   const float n2 = norm2(y);
-  if (n2 > 0.f) {
-    const float ri = rsqrtf(n2);
-    const float m = (amp + lam * (n2 * ri)) * inv1pl;
-    const float sc = m * ri;
-    return cx<float>{y.x * sc, y.y * sc};
-  }
-  return cx<float>{amp * inv1pl, 0.f};
+  const float ri = rsqrt_ftz(fmaxf(n2, 1.17549435e-38f));
+  const float m = (amp + lam * (n2 * ri)) * inv1pl;
+  const cx<float> z = y * (m * ri);
+  return n2 > 0.f ? z : cx<float>{m, 0.f};
 }
 __device__ __forceinline__ float abs_fast_f32(cx<float> a) {
   const float n2 = norm2(a);
-  return n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
+  return n2 * rsqrt_ftz(fmaxf(n2, 1.17549435e-38f));
 }
 
 // Sum a per-thread double over the NT threads of one frame slot; result valid

@@ -156,15 +156,17 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   T pa[RC];
   auto prefetch = [&](int ff, int grp) {
     if (ff >= a.nframes) return;
-    const int x = grp * CG + cx_;
-    const int64_t base = static_cast<int64_t>(ff) * S * S + x;
+    // one base pointer per array; the (ky - gc) * S offsets are immediates
+    const int64_t base = static_cast<int64_t>(ff) * S * S + gc * S + grp * CG + cx_;
+    const cx<T>* gsrc = a.gamma_in + base;
+    const T* asrc = a.amp + base;
 #pragma unroll
     for (int q = 0; q < RC / GC; ++q)
 #pragma unroll
       for (int k1 = 0; k1 < GC; ++k1) {
-        const int ky = gc + GC * q + RC * k1;
-        if constexpr (!FWD) pg[q * GC + k1] = a.gamma_in[base + static_cast<int64_t>(ky) * S];
-        if (!FWD || a.rf_part) pa[q * GC + k1] = a.amp[base + static_cast<int64_t>(ky) * S];
+        const int oy = GC * q + RC * k1;
+        if constexpr (!FWD) pg[q * GC + k1] = gsrc[oy * S];
+        if (!FWD || a.rf_part) pa[q * GC + k1] = asrc[oy * S];
       }
   };
   prefetch(blockIdx.x, 0);
@@ -252,14 +254,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
       // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
       T acc = T(0);
+      const int64_t fx = fbase + gc * S + x;  // + (ky - gc) * S below, immediates
       if constexpr (FWD) {
 #pragma unroll
         for (int q = 0; q < RC / GC; ++q)
 #pragma unroll
           for (int k1 = 0; k1 < GC; ++k1) {
             const int e = q * GC + k1;
-            const int ky = gc + GC * q + RC * k1;
-            const int64_t idx = fbase + static_cast<int64_t>(ky) * S + x;
+            const int64_t idx = fx + (GC * q + RC * k1) * S;
             const cx<T> au = w[e] * scale;
             if (a.frames_out) a.frames_out[idx] = au;
             if (a.inten_out) a.inten_out[idx] = norm2(au);
@@ -278,8 +280,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int k1 = 0; k1 < GC; ++k1) {
           const int e = q * GC + k1;
-          const int ky = gc + GC * q + RC * k1;
-          const int64_t idx = fbase + static_cast<int64_t>(ky) * S + x;
+          const int64_t idx = fx + (GC * q + RC * k1) * S;
           const cx<T> au = w[e] * scale;
           const cx<T> yv = pg[e] + au;
           cx<T> z;

@@ -272,6 +272,7 @@ class Blind final : public BlindGpu {
     a.lam = static_cast<T>(cfg_.eta);
     a.eps = static_cast<T>(cfg_.epsilon);
     a.fast_prox = cfg_.eta <= (1.0 - cfg_.epsilon) / cfg_.epsilon;
+    R.set_pieces(a);  // streamed sweep schedule (one piece per frame: q_j stays per frame)
     PDD_CUDA(launch_frame<T>(kBlind, R.S, a, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
     R.reduce_rf(true);

@@ -104,6 +104,7 @@ struct RankData {
   DevMem fr_off, fr_pitch, fr_r, fr_c, fr_sub;
   DevMem tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg, psides, pgeom;
   DevMem sub_fr_beg, sub_tile_beg, local_map;
+  DevMem pc_beg, pc_pos, pc_ofs, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
   DevMem ctl, rec;
   DevMem pin_dev;  // uint8 per local image pixel
@@ -121,13 +122,14 @@ struct RankData {
   int* skipA() const { return &ctl.as<RunCtl>()->skipA; }
   int* skipB() const { return &ctl.as<RunCtl>()->skipB; }
 
+  // piece_len > 1: multi-frame back-projection pieces for the streamed sweep (layout.hpp)
   void build(const Plan& plan, const DataSpec& data, const double* pin_ones, int dev, Comm* c, int max_iters,
-             const char* who) {
+             const char* who, int piece_len = 1) {
     device = dev;
     comm = c;
     const int rank = c ? c->rank() : 0, world = c ? c->world() : 1;
     SetupTimer tm;
-    L = Layout::build(plan, rank, world, sizeof(T) == 4);
+    L = Layout::build(plan, rank, world, sizeof(T) == 4, piece_len);
     tm.mark("layout");
     S = L.S;
     D = plan.D;
@@ -138,9 +140,10 @@ struct RankData {
     cudaStream_t s = st();
     tw = upload(twiddles<T>(S), s);
     fr_off = upload(L.fr_off, s);
-    rows_al16 = (sizeof(cx<T>) >= 16) ||
-                (std::all_of(L.fr_off.begin(), L.fr_off.end(), [](int64_t o) { return o % 2 == 0; }) &&
-                 std::all_of(L.fr_pitch.begin(), L.fr_pitch.end(), [](int32_t p) { return p % 2 == 0; }));
+    rows_al16 = ((sizeof(cx<T>) >= 16) ||
+                 (std::all_of(L.fr_off.begin(), L.fr_off.end(), [](int64_t o) { return o % 2 == 0; }) &&
+                  std::all_of(L.fr_pitch.begin(), L.fr_pitch.end(), [](int32_t p) { return p % 2 == 0; }))) &&
+                !std::getenv("PDD_NO_TMA_ROWS");  // debug: plain loads for the patch rows
     fr_pitch = upload(L.fr_pitch, s);
     fr_r = upload(L.fr_r, s);
     fr_c = upload(L.fr_c, s);
@@ -156,6 +159,20 @@ struct RankData {
     sub_fr_beg = upload(L.sub_fr_beg, s);
     sub_tile_beg = upload(L.sub_tile_beg, s);
     local_map = upload(L.local_subs, s);
+    if (const int G = sweep_stream_ctas<T>(S); G > 0) {  // the streamed sweep's schedule
+      L.schedule(G);
+      pc_beg = upload(L.cta_beg, s);
+      pc_pos = upload(L.cta_pos, s);
+      pc_ofs = upload(L.cta_ofs, s);
+    }
+    if (L.chained) {
+      it_r = upload(L.it_r, s);
+      it_c = upload(L.it_c, s);
+      it_h = upload(L.it_h, s);
+      it_base = upload(L.it_base, s);
+      tile_items = upload(L.tile_items, s);
+      tile_item_beg = upload(L.tile_item_beg, s);
+    }
     rf_part.alloc(sizeof(double) * std::max<int64_t>(L.nfr, 1));
     re_part.alloc(sizeof(double) * 2 * std::max(L.ntiles(), 1));
     sums.alloc(sizeof(double) * 3 * D);
@@ -279,7 +296,26 @@ struct RankData {
     a.amp = amp.as<T>();
     a.scale = static_cast<T>(1.0 / static_cast<double>(S));
     a.rows_al16 = rows_al16 ? 1 : 0;
+    a.img_elems = L.img_elems;
     return a;
+  }
+
+  // The streamed sweep's pieces / the update gather's partial images (chained layouts only).
+  void set_pieces(FrameArgs<T>& a) const {
+    if (!L.ncta) return;
+    a.cta_beg = pc_beg.as<int32_t>();
+    a.ncta = L.ncta;
+    a.pc_pos = pc_pos.as<int4>();
+    a.pc_ofs = pc_ofs.as<int64_t>();
+  }
+  void set_pieces(GatherArgs<T>& g) const {
+    if (!L.chained) return;
+    g.tile_items = tile_items.as<int32_t>();
+    g.tile_item_beg = tile_item_beg.as<int32_t>();
+    g.it_r = it_r.as<int32_t>();
+    g.it_c = it_c.as<int32_t>();
+    g.it_h = it_h.as<int32_t>();
+    g.it_base = it_base.as<int64_t>();
   }
 
   GatherArgs<T> gather_args(int mode) const {

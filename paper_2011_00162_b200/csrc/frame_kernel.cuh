@@ -49,6 +49,15 @@ struct FrameArgs {
   unsigned long long* phase_cycles = nullptr;  // PDD_PHASE_TIMING builds: per-phase SM cycles
   int rows_al16 = 0;                  // every window row starts 16-byte aligned (streamed kernel: TMA rows)
   int bp_raw = 0;                     // SWEEP: bp_out = IFFT(.) without conj(probe) (the blind q_j)
+  // Streamed sweep schedule (required by the streamed SWEEP kernel; layout.hpp):
+  // CTA b of ncta runs positions [cta_beg[b], cta_beg[b+1]), frames in
+  // back-projection piece order.  Unchained layouts: one piece per frame,
+  // written whole to bp_out + f * S * S.
+  const int32_t* cta_beg = nullptr;   // [ncta+1]
+  int ncta = 0;
+  const int4* pc_pos = nullptr;       // [nframes] {frame, lo, newfrom, rot}
+  const int64_t* pc_ofs = nullptr;    // [nframes]
+  int64_t img_elems = 0;              // PDD_BOUNDS builds: image buffer size (elements)
 };
 
 // ST-AGM per-pixel prox, stagm.cpp:45-73.  amp = sqrt(b).  The fast form is

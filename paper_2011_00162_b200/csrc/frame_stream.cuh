@@ -21,10 +21,15 @@
 // no_instructions in its ncu capture).
 #pragma once
 
+#include <cstdio>
 #include <type_traits>
 
 #include "frame_kernel.cuh"
 #include "tmem.cuh"
+
+#ifndef PDD_ACC_ON
+#define PDD_ACC_ON true  // tensor-memory back-projection accumulation (false: A/B builds)
+#endif
 
 namespace pdd {
 
@@ -55,7 +60,24 @@ struct ProbeTmem {
   static constexpr int RAW = PER_THREAD * SLOTS;
   static constexpr int NCOLS = RAW <= 32 ? 32 : RAW <= 64 ? 64 : RAW <= 128 ? 128 : RAW <= 256 ? 256 : 512;
   static_assert(RAW <= 512, "probe does not fit in TMEM");
+  // Back-projection accumulator ring after the probe: per thread (image row
+  // Y mod 16, column residue g) 8 ring slots of 16-row bands x RR complex.
+  static constexpr int ACC0 = NCOLS;
+  static constexpr int ACC_COLS = 8 * 2 * SH::RR;
+  static constexpr int NCOLS_ACC = ACC0 + ACC_COLS;
 };
+
+#ifndef PDD_STAGE64
+#define PDD_STAGE64 0  // A/B builds: stage the S = 64 amplitudes too
+#endif
+// Which shapes stage the column group's amplitudes in shared memory.
+template <typename T, class SH, bool FWD>
+constexpr bool amp_tile_staged() {
+  return (SH::S == 128 || PDD_STAGE64) && std::is_same_v<T, float>;
+}
+
+template <typename T, class SH>
+constexpr size_t stream_smem_bytes_base();
 
 // FWD = true: the forward half only (FrameMode kFwd: A u -> frames_out,
 // |A u|^2 -> inten_out, R-factor partials), e.g. the trailing R-factor pass.
@@ -66,22 +88,34 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
   cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
-  cx<T>* buf = twr + S;
+  cx<T>* twc = twr + S;  // column-phase twiddles, [gc][k] = W_S^(gc k): immediate offsets in k
+  cx<T>* buf = twc + S;
   double* red = reinterpret_cast<double*>(buf + S * P);
+  // S = 128: the amplitudes of the next column group land by cp.async straight
+  // in shared memory ([element][thread], conflict-free, read back only by the
+  // thread that copied them) -- the column phase sits at the 128-register cap
+  // and a register prefetch spilled.
+  T* ampst = reinterpret_cast<T*>(red + NT / 32);
 
   if (a.stop_flag && *a.stop_flag) return;
   const int t = threadIdx.x;
   for (int i = t; i < S; i += NT) {
     tw[i] = a.tw[i];
     twr[i] = a.tw[(i % GR) * (i / GR)];
+    twc[i] = a.tw[(i / RC) * (i % RC)];
   }
 
   __shared__ uint32_t tmem_slot;
   uint32_t tmem_base = 0;
   const int warp = t >> 5;
+  // tensor-memory back-projection accumulation across the frames of a piece
+  // (S = 128: the 16-row ring maps an image row to a fixed lane, see layout.hpp)
+  constexpr bool ACC = PDD_ACC_ON && TMEMP && !FWD && S == 128 && SH::GR == 8;
+  constexpr int TCOLS = ACC ? 512 : ProbeTmem<SH>::NCOLS;
+  if constexpr (ACC) static_assert(ProbeTmem<SH>::NCOLS_ACC <= 512, "TMEM: probe + accumulator");
   if constexpr (TMEMP) {
     static_assert(std::is_same_v<T, float> && 2 * RR == 32, "TMEM probe path: float, 16 values per row batch");
-    if (warp == 0) tmem_alloc<ProbeTmem<SH>::NCOLS>(&tmem_slot);
+    if (warp == 0) tmem_alloc<TCOLS>(&tmem_slot);
     tmem_fence_before_sync();
     __syncthreads();
     tmem_fence_after_sync();
@@ -142,6 +176,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     __syncwarp();
     if (lane < SH::RW) {
       const int y = rb * RPB + SH::RW * warp + lane;
+#ifdef PDD_BOUNDS
+      if (ff < 0 || ff >= a.nframes || a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff] + S > a.img_elems ||
+          ((a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff]) & 1)) {
+        printf("PDD_BOUNDS issue_rows: cta %d ff %d y %d off %lld pitch %d\n", blockIdx.x, ff, y,
+               (long long)(ff >= 0 && ff < a.nframes ? a.off[ff] : -1), ff >= 0 && ff < a.nframes ? a.pitch[ff] : -1);
+        __trap();
+      }
+#endif
       bulk_g2s(buf + y * P, a.img + a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff], S * sizeof(cx<T>), bar);
     }
   };
@@ -153,9 +195,20 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
   // Prefetch registers: Gamma and amplitude of one column group.
   cx<T> pg[RC];
-  T pa[RC];
+  constexpr bool STAGE = amp_tile_staged<T, SH, FWD>();
+  T pa[STAGE ? 1 : RC];
+  auto pa_at = [&](int e) {
+    if constexpr (STAGE) return ampst[e * NT + t];
+    else return pa[e];
+  };
   auto prefetch = [&](int ff, int grp) {
-    if (ff >= a.nframes) return;
+    if (ff < 0) return;
+#ifdef PDD_BOUNDS
+    if (ff >= a.nframes) {
+      printf("PDD_BOUNDS prefetch: cta %d ff %d grp %d\n", blockIdx.x, ff, grp);
+      __trap();
+    }
+#endif
     // one base pointer per array; the (ky - gc) * S offsets are immediates
     const int64_t base = static_cast<int64_t>(ff) * S * S + gc * S + grp * CG + cx_;
     const cx<T>* gsrc = a.gamma_in + base;
@@ -166,13 +219,36 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k1 = 0; k1 < GC; ++k1) {
         const int oy = GC * q + RC * k1;
         if constexpr (!FWD) pg[q * GC + k1] = gsrc[oy * S];
-        if (!FWD || a.rf_part) pa[q * GC + k1] = asrc[oy * S];
+        if (!FWD || a.rf_part) {
+          if constexpr (STAGE) cp_async4(ampst + (q * GC + k1) * NT + t, asrc + oy * S);
+          else pa[q * GC + k1] = asrc[oy * S];
+        }
       }
+    if constexpr (STAGE) cp_async_commit();
   };
-  prefetch(blockIdx.x, 0);
-  if (tma_rows && blockIdx.x < a.nframes)
+#ifdef PDD_CANARY  // debug builds: detect shared-memory writes past the working set
+  uint32_t* canary = reinterpret_cast<uint32_t*>(smem_raw + stream_smem_bytes_base<T, SH>());
+  for (int k = t; k < (48 << 10) / 4; k += NT) canary[k] = 0xDEADBEEFu;
+  __syncthreads();
+#endif
+  // Work order.  SWEEP: this CTA's positions [cta_beg[b], cta_beg[b+1]) of the
+  // host schedule (frames in back-projection piece order; layout.hpp).
+  // FWD: frames blockIdx.x + k * gridDim.x.
+  int i = FWD ? static_cast<int>(blockIdx.x) : a.cta_beg[blockIdx.x];
+  const int iend = FWD ? a.nframes : a.cta_beg[blockIdx.x + 1];
+  constexpr int kStepOne = 1;
+  auto frame_at = [&](int j) {
+    if constexpr (FWD) return j < iend ? j : -1;
+    else return j < iend ? a.pc_pos[j].x : -1;
+  };
+  auto next_of = [&](int j) { return FWD ? j + static_cast<int>(gridDim.x) : j + kStepOne; };
+  {
+    const int f0 = frame_at(i);
+    prefetch(f0, 0);
+    if (tma_rows && f0 >= 0)
 #pragma unroll 1
-    for (int rb = 0; rb < NRB; ++rb) issue_rows(blockIdx.x, rb);
+      for (int rb = 0; rb < NRB; ++rb) issue_rows(f0, rb);
+  }
 
 #ifdef PDD_PHASE_TIMING
   unsigned long long tph[4] = {0, 0, 0, 0};
@@ -188,8 +264,15 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   do {              \
   } while (0)
 #endif
-  for (int f = blockIdx.x; f < a.nframes; f += gridDim.x) {
+  for (; i < iend; i = next_of(i)) {
+    const int f = frame_at(i);
     const int64_t fbase = static_cast<int64_t>(f) * S * S;
+#ifdef PDD_BOUNDS
+    if (f < 0 || f >= a.nframes) {
+      printf("PDD_BOUNDS frame: cta %d i %d iend %d f %d\n", blockIdx.x, i, iend, f);
+      __trap();
+    }
+#endif
     // ---------------- rows, forward
 #pragma unroll 1
     for (int rb = 0; rb < NRB; ++rb) {
@@ -243,7 +326,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
       dft<RC, false>(w);
 #pragma unroll
-      for (int k = 0; k < RC; ++k) buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * tw[gc * k];
+      for (int k = 0; k < RC; ++k) buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * twc[gc * RC + k];
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
@@ -253,6 +336,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         dft<GC, false>(w + q * GC);
       }
       // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
+      if constexpr (STAGE) cp_async_wait_all();  // this thread's staged amplitudes
       T acc = T(0);
       const int64_t fx = fbase + gc * S + x;  // + (ky - gc) * S below, immediates
       if constexpr (FWD) {
@@ -266,13 +350,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
             if (a.frames_out) a.frames_out[idx] = au;
             if (a.inten_out) a.inten_out[idx] = norm2(au);
             if (a.rf_part) {
-              if constexpr (FAST && std::is_same_v<T, float>) acc += fabsf(abs_fast_f32(au) - pa[e]);
-              else acc += fabs(sqrt(norm2(au)) - pa[e]);
+              if constexpr (FAST && std::is_same_v<T, float>) acc += fabsf(abs_fast_f32(au) - pa_at(e));
+              else acc += fabs(sqrt(norm2(au)) - pa_at(e));
             }
           }
         rf_acc += acc;
         if (grp + 1 < NG) prefetch(f, grp + 1);
-        else prefetch(f + gridDim.x, 0);
+        else prefetch(frame_at(next_of(i)), 0);
         continue;  // groups own disjoint columns of buf: no barrier between them
       }
 #pragma unroll
@@ -285,11 +369,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
           const cx<T> yv = pg[e] + au;
           cx<T> z;
           if constexpr (FAST && std::is_same_v<T, float>) {
-            acc += fabsf(abs_fast_f32(au) - pa[e]);
-            z = prox_fast_f32(yv, pa[e], a.lam, inv1pl);
+            acc += fabsf(abs_fast_f32(au) - pa_at(e));
+            z = prox_fast_f32(yv, pa_at(e), a.lam, inv1pl);
           } else {
-            acc += fabs(sqrt(norm2(au)) - pa[e]);
-            z = stagm_prox(yv, pa[e], a.lam, a.eps, FAST);
+            acc += fabs(sqrt(norm2(au)) - pa_at(e));
+            z = stagm_prox(yv, pa_at(e), a.lam, a.eps, FAST);
           }
           const cx<T> gn = yv - z;
           a.gamma_out[idx] = gn;
@@ -298,7 +382,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         }
       rf_acc += acc;
       if (grp + 1 < NG) prefetch(f, grp + 1);
-      else prefetch(f + gridDim.x, 0);
+      else prefetch(frame_at(next_of(i)), 0);
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
         const int k2 = gc + GC * q;
@@ -310,7 +394,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int k = 0; k < RC; ++k) {
         const cx<T> v = buf[(k * GC + gc) * P + x];
-        w[k] = (k == 0) ? v : mul_conj(v, tw[gc * k]);
+        w[k] = (k == 0) ? v : mul_conj(v, twc[gc * RC + k]);
       }
       dft<RC, true>(w);
 #pragma unroll
@@ -320,6 +404,24 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     PDD_TICK(1);
 
     // ---------------- rows, inverse -> x conj(probe) -> back-projection tile
+    // this frame's piece bookkeeping: rows y < lo are final, rows y >= newfrom new
+    int p_lo = S, p_new = 0, p_rot = 0;
+    int64_t p_ofs = fbase;
+    if constexpr (!FWD) {
+      const int4 pi = a.pc_pos[i];
+      p_lo = pi.y;
+      p_new = pi.z;
+      p_rot = pi.w;
+      p_ofs = a.pc_ofs[i];
+    }
+    const int fn = frame_at(next_of(i));
+#ifdef PDD_BOUNDS
+    if (p_ofs < 0 || p_lo <= 0 || p_lo > S || p_new < 0 || p_new > S || fn >= a.nframes) {
+      printf("PDD_BOUNDS piece: cta %d i %d f %d ofs %lld lo %d new %d fn %d\n", blockIdx.x, i, f, (long long)p_ofs, p_lo,
+             p_new, fn);
+      __trap();
+    }
+#endif
 #pragma unroll 1
     for (int rb = 0; rb < (FWD ? 0 : NRB); ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
@@ -345,21 +447,44 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         const cx<T> b = buf[y * P + k * GR + ((g + k) & (GR - 1))];
         v[k] = (k == 0) ? b : mul_conj(b, twr[k * GR + g]);
       }
-      if (tma_rows && f + static_cast<int>(gridDim.x) < a.nframes) {
+      if (tma_rows && fn >= 0) {
         __syncwarp();             // this warp's rows are consumed
         fence_proxy_async_smem();  // ... before the async proxy overwrites them
-        issue_rows(f + gridDim.x, rb);
+        issue_rows(fn, rb);
       }
       dft<RR, true>(v);
-      cx<T>* dst = a.bp_out + fbase + y * S + g;
-#pragma unroll
       if (a.bp_raw) {  // blind: q_j = IFFT(.) itself; conj(W^{n+1}) is applied in the gather
 #pragma unroll
-        for (int m = 0; m < RR; ++m) dst[GR * m] = v[m] * scale;
+        for (int m = 0; m < RR; ++m) v[m] = v[m] * scale;
       } else {
 #pragma unroll
-        for (int m = 0; m < RR; ++m) dst[GR * m] = mul_conj(v[m] * scale, pv[m]);
+        for (int m = 0; m < RR; ++m) v[m] = mul_conj(v[m] * scale, pv[m]);
       }
+      if constexpr (ACC) {
+        // warp-uniform: p_lo, p_new are multiples of 4 and a warp holds 4 rows
+        const uint32_t ta = tmem_addr(tmem_base, warp, ProbeTmem<SH>::ACC0 + (((y >> 4) + p_rot) & 7) * (2 * RR));
+        if (y < p_new) {  // rows already holding earlier frames of the piece
+          uint32_t raw[32];
+          tmem_ld32(ta, raw);
+          tmem_wait_ld();
+#pragma unroll
+          for (int m = 0; m < RR; ++m) v[m] = v[m] + cx<T>{__uint_as_float(raw[2 * m]), __uint_as_float(raw[2 * m + 1])};
+        }
+        if (y >= p_lo) {  // later frames of the piece still add to this row
+          uint32_t raw[32];
+#pragma unroll
+          for (int m = 0; m < RR; ++m) {
+            raw[2 * m] = __float_as_uint(v[m].x);
+            raw[2 * m + 1] = __float_as_uint(v[m].y);
+          }
+          tmem_st32(ta, raw);
+          tmem_wait_st();
+          continue;
+        }
+      }
+      cx<T>* dst = a.bp_out + p_ofs + y * S + g;
+#pragma unroll
+      for (int m = 0; m < RR; ++m) dst[GR * m] = v[m];
     }
 
     PDD_TICK(2);
@@ -371,7 +496,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int o = 16; o > 0; o >>= 1) rf += __shfl_down_sync(0xffffffffu, rf, o);
       if ((t & 31) == 0) red[t >> 5] = rf;
     }
+    if constexpr (ACC) tmem_fence_before_sync();  // accumulator rows change warps between frames
     __syncthreads();  // also: rows of the next frame overwrite buf
+    if constexpr (ACC) tmem_fence_after_sync();
     if (a.rf_part && t == 0) {
       double s = 0.0;
       for (int w = 0; w < NT / 32; ++w) s += red[w];
@@ -379,6 +506,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
     PDD_TICK(3);
   }
+#ifdef PDD_CANARY
+  __syncthreads();
+  for (int k = t; k < (48 << 10) / 4; k += NT)
+    if (canary[k] != 0xDEADBEEFu) {
+      printf("PDD_CANARY cta %d: word %d past the end = %08x\n", blockIdx.x, k, canary[k]);
+      break;
+    }
+#endif
 #ifdef PDD_PHASE_TIMING
   if (a.phase_cycles && t == 0)
     for (int i = 0; i < 4; ++i) atomicAdd(a.phase_cycles + i, tph[i]);
@@ -388,13 +523,23 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     tmem_fence_before_sync();
     __syncthreads();
     tmem_fence_after_sync();
-    if (warp == 0) tmem_dealloc<ProbeTmem<SH>::NCOLS>(tmem_base);
+    if (warp == 0) tmem_dealloc<TCOLS>(tmem_base);
   }
 }
 
 template <typename T, class SH>
+constexpr size_t stream_smem_bytes_base() {
+  return sizeof(cx<T>) * (3 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32) +
+         (amp_tile_staged<T, SH, false>() ? sizeof(T) * static_cast<size_t>(SH::RC) * SH::NT : 0);
+}
+template <typename T, class SH>
 size_t stream_smem_bytes() {
-  return sizeof(cx<T>) * (2 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32);
+  return sizeof(cx<T>) * (3 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32) +
+         (amp_tile_staged<T, SH, false>() ? sizeof(T) * static_cast<size_t>(SH::RC) * SH::NT : 0)
+#ifdef PDD_CANARY
+         + (size_t(48) << 10)  // debug builds: a canary region after the working set
+#endif
+      ;
 }
 
 }  // namespace pdd

@@ -69,10 +69,40 @@ static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
     if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
   }
   if (a.nframes <= 0) return cudaSuccess;
-  const int grid = std::min(a.nframes, blocks_per_sm * sms);
+  // SWEEP runs the host schedule, built for exactly this grid
+  if (!FWD && (!a.cta_beg || a.ncta != blocks_per_sm * sms)) return cudaErrorInvalidConfiguration;
+  const int grid = FWD ? std::min(a.nframes, blocks_per_sm * sms) : a.ncta;
   kern<<<grid, SH::NT, smem, st>>>(a);
   return cudaGetLastError();
 }
+
+// Persistent grid of the streamed SWEEP kernel for side S (0: not streamed);
+// the host builds the back-projection piece schedule for exactly this grid.
+template <typename T>
+int sweep_stream_ctas(int S) {
+  auto q = [](auto kern, int nt, size_t smem) {
+    int bps = 0, sms = 0, dev = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, nt, smem) != cudaSuccess)
+      return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return bps * sms;
+  };
+  if constexpr (std::is_same_v<T, float>) {
+    if (S == 128) {
+      using SH = StreamPick<float, 128>::type;
+      return q(sweep_stream_kernel<float, SH, true, SH::MINB == 1, false>, SH::NT, stream_smem_bytes<float, SH>());
+    }
+    if (S == 64) {
+      using SH = StreamPick<float, 64>::type;
+      return q(sweep_stream_kernel<float, SH, true, SH::MINB == 1, false>, SH::NT, stream_smem_bytes<float, SH>());
+    }
+  }
+  return 0;
+}
+template int sweep_stream_ctas<float>(int);
+template int sweep_stream_ctas<double>(int);
 
 template <typename T, int S, int MODE>
 static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
@@ -220,10 +250,15 @@ template <typename T, int NROW, int VEC, int MODE>
 __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGatherAdjoint) ? 4 : 1) gather_kernel(const GatherArgs<T> a) {
   constexpr int kMeta = 256;  // covering frames staged in shared memory per chunk
   __shared__ double sm[16];
-  __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta];
+  __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta], s_h[kMeta];
+  __shared__ int64_t s_base[kMeta];
   if (a.stop_flag && *a.stop_flag) return;
   const int4 td = a.tiles[blockIdx.x];
-  const int sub = td.x, tr0 = td.y, tc0 = td.z, fb = td.w, fe = a.tiles[blockIdx.x + 1].w;
+  const int sub = td.x, tr0 = td.y, tc0 = td.z;
+  // covering partial images: back-projection pieces, or frames
+  const bool items = (MODE == kGatherNonblind || MODE == kGatherAdjoint) && a.tile_items != nullptr;
+  const int fb = items ? a.tile_item_beg[blockIdx.x] : td.w;
+  const int fe = items ? a.tile_item_beg[blockIdx.x + 1] : a.tiles[blockIdx.x + 1].w;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int H = a.sub_h[sub], W = a.sub_w[sub];
   const int c = tc0 + VEC * tx;  // first of this lane's VEC columns
@@ -252,26 +287,38 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
     const int nk = min(kMeta, nf - kb);
     if (kb > 0) __syncthreads();
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-      const int fr = a.tile_frames[fb + kb + k];
-      s_fr[k] = fr;
-      s_r0[k] = a.fr_r[fr];
-      s_c0[k] = a.fr_c[fr];
+      if (items) {
+        const int it = a.tile_items[fb + kb + k];
+        s_fr[k] = -1;
+        s_r0[k] = a.it_r[it];
+        s_c0[k] = a.it_c[it];
+        s_h[k] = a.it_h[it];
+        s_base[k] = a.it_base[it];
+      } else {
+        const int fr = a.tile_frames[fb + kb + k];
+        s_fr[k] = fr;
+        s_r0[k] = a.fr_r[fr];
+        s_c0[k] = a.fr_c[fr];
+        s_h[k] = S;
+        s_base[k] = fr * SS;
+      }
     }
     __syncthreads();
     if constexpr (MODE == kGatherAdjoint || MODE == kGatherNonblind) {
       // plain overlap-add: U frames x NROW rows of loads issued as one batch,
       // then added in ascending frame order
       using V = typename Vec2<T>::type;
-      constexpr int U = 4;
       constexpr int NV = (VEC == 2 && std::is_same_v<T, float>) ? 1 : VEC;  // loads per row
+      // frames per batch: about 8 loads in flight per thread (64-register cap)
+      constexpr int U = (NROW * NV >= 4) ? 2 : 8 / (NROW * NV);
       using L = std::conditional_t<NV == 1 && VEC == 2, float4, V>;
       auto load = [&](int k, int i, int v) -> L {
         const int cc = c - s_c0[k];
         const int rr = tr0 + ty + 8 * i - s_r0[k];
         const bool ok = static_cast<unsigned>(cc) < static_cast<unsigned>(S) &&
-                        static_cast<unsigned>(rr) < static_cast<unsigned>(S);
+                        static_cast<unsigned>(rr) < static_cast<unsigned>(s_h[k]);
         L q{};
-        if (ok) q = __ldcs(reinterpret_cast<const L*>(a.bp + s_fr[k] * SS + static_cast<int64_t>(rr) * S + cc + v));
+        if (ok) q = __ldcs(reinterpret_cast<const L*>(a.bp + s_base[k] + static_cast<int64_t>(rr) * S + cc + v));
         return q;
       };
       auto add = [&](int i, int v, const L& q) {

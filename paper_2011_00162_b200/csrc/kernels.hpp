@@ -38,6 +38,15 @@ struct GatherArgs {
   const int32_t* fr_r = nullptr;        // [nframes] window corner (subdomain coords)
   const int32_t* fr_c = nullptr;
   const int32_t* fr_sub = nullptr;      // [nframes] owning local subdomain
+  // Nonblind update over back-projection pieces (layout.hpp) instead of
+  // frames: partial image k is [it_h[k]][S] at bp + it_base[k], window corner
+  // (it_r[k], it_c[k]); per tile the covering pieces tile_items[tile_item_beg[t] ..].
+  const int32_t* tile_items = nullptr;
+  const int32_t* tile_item_beg = nullptr;
+  const int32_t* it_r = nullptr;
+  const int32_t* it_c = nullptr;
+  const int32_t* it_h = nullptr;
+  const int64_t* it_base = nullptr;
   int S = 0;
   const cx<T>* bp = nullptr;            // [nframes][S][S]
   const cx<T>* probe = nullptr;         // density: P; blind: W copies [nsub][S][S]
@@ -72,6 +81,8 @@ struct PairGeom {
 
 template <typename T>
 cudaError_t launch_frame(int mode, int S, const FrameArgs<T>& a, cudaStream_t st);
+template <typename T>
+int sweep_stream_ctas(int S);  // persistent grid of the streamed SWEEP kernel (0: not streamed)
 template <typename T>
 bool frame_supported(int S);
 

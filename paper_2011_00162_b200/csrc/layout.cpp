@@ -4,7 +4,7 @@
 
 namespace pdd {
 
-Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide) {
+Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int piece_len) {
   Layout L;
   L.D = plan.D;
   L.rank = rank;
@@ -70,6 +70,104 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide) {
   }
   L.tiles.push_back(int4{0, 0, 0, static_cast<int>(L.tile_frames.size())});
 
+  // back-projection pieces (see layout.hpp)
+  const bool chain = piece_len > 1;
+  L.chained = chain;
+  L.piece_len = std::max(1, std::min(piece_len, kPieceLen));
+  L.pc_beg.push_back(0);
+  const int64_t S = L.S;
+  auto add_piece = [&](const std::vector<int64_t>& fs) {
+    const int64_t r0 = L.fr_r[fs[0]], h = L.fr_r[fs.back()] - r0 + S;
+    const int64_t base = L.part_elems;
+    for (size_t i = 0; i < fs.size(); ++i) {
+      const int64_t r = L.fr_r[fs[i]];
+      const int lo = i + 1 < fs.size() ? static_cast<int>(L.fr_r[fs[i + 1]] - r) : static_cast<int>(S);
+      const int nf = i > 0 ? static_cast<int>(S - (r - L.fr_r[fs[i - 1]])) : 0;
+      L.pc_pos.push_back(int4{static_cast<int>(fs[i]), lo, nf, static_cast<int>((r >> 4) & 7)});
+      L.pc_ofs.push_back(base + (r - r0) * S);
+    }
+    L.pc_beg.push_back(static_cast<int32_t>(L.pc_pos.size()));
+    L.it_r.push_back(static_cast<int32_t>(r0));
+    L.it_c.push_back(L.fr_c[fs[0]]);
+    L.it_h.push_back(static_cast<int32_t>(h));
+    L.it_base.push_back(base);
+    L.part_elems += h * S;
+  };
+  for (int ld = 0; ld < L.nls(); ++ld) {
+    const int64_t fb = L.sub_fr_beg[ld], fe = L.sub_fr_beg[ld + 1];
+    if (!chain) {
+      for (int64_t f = fb; f < fe; ++f) add_piece({f});
+      continue;
+    }
+    // runs per window column (ascending row), split where the spacing breaks
+    // the ring (not a positive multiple of 16 up to S), then cut into
+    // ceil(n / piece_len) pieces of near-equal length
+    std::vector<int64_t> order;
+    for (int64_t f = fb; f < fe; ++f) order.push_back(f);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      return L.fr_c[a] != L.fr_c[b] ? L.fr_c[a] < L.fr_c[b] : L.fr_r[a] < L.fr_r[b];
+    });
+    std::vector<std::vector<int64_t>> runs;
+    for (int64_t f : order) {
+      bool join = !runs.empty();
+      if (join) {
+        const auto& cur = runs.back();
+        const int64_t pf = cur.back(), d = L.fr_r[f] - L.fr_r[pf];
+        join = L.fr_c[f] == L.fr_c[pf] && d > 0 && d <= S && d % 16 == 0;
+      }
+      if (join) runs.back().push_back(f);
+      else runs.push_back({f});
+    }
+    {
+      std::vector<std::vector<int64_t>> cut;
+      for (const auto& r : runs) {
+        const int64_t n = static_cast<int64_t>(r.size()), k = (n + L.piece_len - 1) / L.piece_len;
+        for (int64_t p = 0, b = 0; p < k; ++p) {
+          const int64_t e = (n * (p + 1)) / k;
+          cut.emplace_back(r.begin() + b, r.begin() + e);
+          b = e;
+        }
+      }
+      runs.swap(cut);
+    }
+    // sweep order: by first row, then column -- concurrently running CTAs
+    // then work on horizontally adjacent pieces and share the image rows in L2
+    std::stable_sort(runs.begin(), runs.end(), [&](const auto& a, const auto& b) {
+      return L.fr_r[a[0]] != L.fr_r[b[0]] ? L.fr_r[a[0]] < L.fr_r[b[0]] : L.fr_c[a[0]] < L.fr_c[b[0]];
+    });
+    for (const auto& r : runs) add_piece(r);
+  }
+  // covering pieces per gather tile, (column, row) order
+  {
+    const int th = L.tile_h, tw = L.tile_w;
+    L.tile_item_beg.push_back(0);
+    int k0 = 0;
+    for (int ld = 0; ld < L.nls(); ++ld) {
+      const int64_t H = L.sub_h[ld], W = L.sub_w[ld];
+      const int64_t ntr = (H + th - 1) / th, ntc = (W + tw - 1) / tw;
+      std::vector<std::vector<int32_t>> lists(static_cast<size_t>(ntr * ntc));
+      int k1 = k0;
+      while (k1 < L.npieces() && L.fr_sub[L.pc_pos[L.pc_beg[k1]].x] == ld) ++k1;
+      std::vector<int32_t> ids;
+      for (int k = k0; k < k1; ++k) ids.push_back(k);
+      std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
+        return L.it_c[a] != L.it_c[b] ? L.it_c[a] < L.it_c[b] : L.it_r[a] < L.it_r[b];
+      });
+      for (int32_t k : ids) {
+        const int64_t r0 = L.it_r[k], c0 = L.it_c[k];
+        const int64_t tr_a = r0 / th, tr_b = std::min(ntr - 1, (r0 + L.it_h[k] - 1) / th);
+        const int64_t tc_a = c0 / tw, tc_b = std::min(ntc - 1, (c0 + S - 1) / tw);
+        for (int64_t tr = tr_a; tr <= tr_b; ++tr)
+          for (int64_t tc = tc_a; tc <= tc_b; ++tc) lists[tr * ntc + tc].push_back(k);
+      }
+      for (const auto& l : lists) {
+        L.tile_items.insert(L.tile_items.end(), l.begin(), l.end());
+        L.tile_item_beg.push_back(static_cast<int32_t>(L.tile_items.size()));
+      }
+      k0 = k1;
+    }
+  }
+
   // overlap pairs touching a local subdomain, ascending global p
   std::vector<int> lp_of(plan.overlaps.size(), -1);
   for (size_t p = 0; p < plan.overlaps.size(); ++p) {
@@ -127,6 +225,21 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide) {
     L.sub_pbeg.push_back(static_cast<int32_t>(L.psides.size()));
   }
   return L;
+}
+
+void Layout::schedule(int G) {
+  ncta = G;
+  cta_beg.assign(1, 0);
+  cta_pos.clear();
+  cta_ofs.clear();
+  for (int b = 0; b < G; ++b) {
+    for (int k = b; k < npieces(); k += G)
+      for (int q = pc_beg[k]; q < pc_beg[k + 1]; ++q) {
+        cta_pos.push_back(pc_pos[q]);
+        cta_ofs.push_back(pc_ofs[q]);
+      }
+    cta_beg.push_back(static_cast<int32_t>(cta_pos.size()));
+  }
 }
 
 }  // namespace pdd

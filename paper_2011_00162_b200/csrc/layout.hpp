@@ -50,6 +50,37 @@ struct Layout {
   std::vector<int32_t> tile_frames;
   std::vector<int64_t> sub_tile_beg;  // [nls+1]
 
+  // Back-projection pieces.  A piece is a run of frames of one subdomain
+  // that share a window column, in ascending rows spaced by a multiple of 16
+  // px (at most S apart, at most kPieceLen frames).  The streamed sweep
+  // (S = 128, float) keeps a piece's running overlap-add in tensor memory and
+  // writes each image row of the piece once, into a [h][S] partial image; the
+  // update gather then sums the pieces covering a pixel in (column, row)
+  // order.  With chaining off every frame is its own piece and the partial
+  // images are the per-frame tiles [nfr][S][S].  Pieces depend only on the
+  // subdomain, so iterates stay identical for every GPU count.
+  static constexpr int kPieceLen = 8;  // upper bound of piece_len
+  bool chained = false;
+  int piece_len = 1;
+  std::vector<int32_t> pc_beg;   // [npieces+1] CSR into pc_pos / pc_ofs (sweep order)
+  std::vector<int4> pc_pos;      // [nfr] {frame, lo, newfrom, rot}: rows y < lo are final after
+                                 // this frame, rows y >= newfrom are first touched by it,
+                                 // rot = (window row / 16) mod 8 (tensor-memory ring slot)
+  std::vector<int64_t> pc_ofs;   // [nfr] element offset of the frame's window row 0 in the partials
+  std::vector<int32_t> it_r, it_c, it_h;  // [npieces] partial image rect (subdomain coords, width S)
+  std::vector<int64_t> it_base;           // [npieces] element offset of the partial image
+  int64_t part_elems = 0;
+  std::vector<int32_t> tile_items;        // per tile: covering pieces, (column, row) order
+  std::vector<int32_t> tile_item_beg;     // [ntiles+1]
+  int npieces() const { return static_cast<int>(pc_beg.size()) - 1; }
+  // Sweep schedule for a persistent grid of G CTAs: pieces k = b, b + G, ...
+  // go to CTA b; its positions are cta_pos[cta_beg[b] .. cta_beg[b+1]).
+  int ncta = 0;
+  std::vector<int32_t> cta_beg;
+  std::vector<int4> cta_pos;
+  std::vector<int64_t> cta_ofs;
+  void schedule(int G);
+
   std::vector<int> lpairs;          // global pair index per local pair
   std::vector<PairGeom> pgeom;      // per local pair
   std::vector<int32_t> sub_pbeg;    // [nls+1] CSR into psides
@@ -58,7 +89,9 @@ struct Layout {
   int max_pair_pix = 0;
   std::vector<Exchange> exch;
 
-  static Layout build(const Plan& plan, int rank, int world, bool allow_wide = false);
+  // piece_len > 1: multi-frame back-projection pieces of at most piece_len
+  // frames (else one piece per frame)
+  static Layout build(const Plan& plan, int rank, int world, bool allow_wide = false, int piece_len = 1);
   int nls() const { return static_cast<int>(local_subs.size()); }
   int ntiles() const { return static_cast<int>(tiles.size()) - 1; }
 };

@@ -12,6 +12,9 @@
 // Two iterations (Gamma parities) per graph.  The R-factor of iterate n is
 // produced by the frame pass of iteration n+1 (its forward transform is the
 // reference's cached `au`), and by one trailing frame pass at the end.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <chrono>
 
 #include "common.cuh"
@@ -36,7 +39,7 @@ class Nonblind final : public NonblindGpu {
       : plan_(plan), cfg_(cfg) {
     cfg_.validate();
     plan.g.validate();
-    R.build(plan, data, pin_ones, device, comm, cfg.max_iters, "NonblindSolver");
+    R.build(plan, data, pin_ones, device, comm, cfg.max_iters, "NonblindSolver", piece_length(plan, device));
     if (R.l1 <= 0.0) throw InvalidArgument("NonblindSolver: all-zero measurements, R-factor undefined");
     const int64_t SS = R.SS();
     cudaStream_t s = R.st();
@@ -45,7 +48,7 @@ class Nonblind final : public NonblindGpu {
     const int64_t nf = R.L.nfr * SS;
     gamma_[0].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
     gamma_[1].alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
-    bp_.alloc(sizeof(cx<T>) * std::max<int64_t>(nf, 1));
+    bp_.alloc(sizeof(cx<T>) * std::max<int64_t>(std::max(nf, R.L.part_elems), 1));  // partials; also A u scratch
     for (int p = 0; p < 2; ++p) {  // iterate ping-pong (state of iteration n in [n & 1])
       u_[p].alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.img_elems, 1));
       v_[p].alloc(sizeof(cx<T>) * std::max<int64_t>(R.L.v_elems, 1));
@@ -61,6 +64,23 @@ class Nonblind final : public NonblindGpu {
   }
 
   const StateLayout& layout() const override { return layout_; }
+
+  // S = 128 float32: the streamed sweep accumulates back-projections over
+  // pieces of frames in tensor memory.  The length depends on the plan and
+  // the device only -- never on the GPU count, so iterates stay identical for
+  // every G: at least 6 pieces per SM when each GPU holds a single subdomain
+  // (the smallest per-GPU share; the static piece schedule then stays within
+  // a few percent of balance), at most Layout::kPieceLen frames.
+  // PDD_PIECE_LEN overrides (1: one piece per frame, for A/B runs).
+  static int piece_length(const Plan& plan, int device) {
+    if (sizeof(T) != 4 || plan.g.s != 128) return 1;
+    if (const char* e = std::getenv("PDD_PIECE_LEN")) return std::max(1, std::atoi(e));
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) return 1;
+    int64_t jmin = INT64_MAX;
+    for (const auto& fr : plan.frames_of) jmin = std::min<int64_t>(jmin, static_cast<int64_t>(fr.size()));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(Layout::kPieceLen, jmin / (6 * int64_t(sms)))));
+  }
 
   // solver.cpp:53-75: denom = eta * illumination_density + r per covering pair.
   void build_denominators() {
@@ -154,6 +174,7 @@ class Nonblind final : public NonblindGpu {
     a.lam = static_cast<T>(cfg_.eta);
     a.eps = static_cast<T>(cfg_.epsilon);
     a.fast_prox = cfg_.eta <= (1.0 - cfg_.epsilon) / cfg_.epsilon;
+    R.set_pieces(a);
     PDD_CUDA(launch_frame<T>(kSweep, R.S, a, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
     R.reduce_rf(true);
@@ -161,6 +182,7 @@ class Nonblind final : public NonblindGpu {
     // v^{n+1} from u^n, Lambda^n (solver.cpp:141-151) into the outgoing parity
     R.consensus(U(parity), LAM(parity), s_.as<cx<T>>(), V(1 - parity), R.skipB());
     GatherArgs<T> g = R.gather_args(kGatherNonblind);
+    R.set_pieces(g);
     g.bp = bp_.as<cx<T>>();
     g.u_in = U(parity);
     g.u = U(1 - parity);

@@ -70,6 +70,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// cp.async (LDGSTS): 4-byte global -> shared copy with no register staging.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // Address of column `col` in the lane quarter of warp `warp` (warp w may only
 // touch lanes 32*(w%4) .. 32*(w%4)+31).
 __device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int col) {

@@ -319,7 +319,7 @@ def main():
                         "frames": J, "parallelism": f"subdomains over {world} GPU(s)",
                         "l2": "inputs > L2 (no flush needed)"},
                 roofline={"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s",
-                          "frac": k1_gbs / peak, "traffic": traffic, "kernel": "frame_kernel SWEEP (K1)",
+                          "frac": k1_gbs / peak, "traffic": traffic, "kernel": "sweep_stream_kernel (K1)",
                           "kernel_ms": ms_frame, "algorithmic_bytes_per_launch": k1_bytes,
                           "peak_kind": peak_kind,
                           "fp32_tflops": fft_flops / (ms_frame / 1e3) / 1e12},

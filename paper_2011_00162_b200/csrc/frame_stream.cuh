@@ -67,6 +67,26 @@ struct ProbeTmem {
   static constexpr int NCOLS_ACC = ACC0 + ACC_COLS;
 };
 
+#ifndef PDD_TW128
+#define PDD_TW128 0  // twiddles by 16-byte shared loads (two per instruction)
+#endif
+#ifndef PDD_ROWFUSE
+#define PDD_ROWFUSE 1  // inverse rows of frame i and forward rows of frame i+1 without a CTA barrier
+#endif
+#ifndef PDD_COLSPLIT
+#define PDD_COLSPLIT 2  // column groups: independent warp sets exchanging through named barriers
+#endif
+
+// Two twiddles W[k], W[k+1] (k even) by one 16-byte shared-memory load.
+__device__ __forceinline__ void tw_pair(const cx<float>* p, cx<float>& a, cx<float>& b) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = cx<float>{v.x, v.y};
+  b = cx<float>{v.z, v.w};
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 #ifndef PDD_STAGE64
 #define PDD_STAGE64 0  // A/B builds: stage the S = 64 amplitudes too
 #endif
@@ -86,6 +106,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 16-byte twiddle loads: float, RR/RC even
+  constexpr bool TWV = PDD_TW128 && std::is_same_v<T, float> && RR % 2 == 0 && RC % 2 == 0;
+  // column phase split into NSPLIT independent warp sets (S = 128 float sweep)
+  constexpr int NSPLIT = (std::is_same_v<T, float> && S == 128 && CG % PDD_COLSPLIT == 0 &&
+                          (NT / 32) % PDD_COLSPLIT == 0) ? PDD_COLSPLIT : 1;
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
   cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
   cx<T>* twc = twr + S;  // column-phase twiddles, [gc][k] = W_S^(gc k): immediate offsets in k
@@ -101,7 +126,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   const int t = threadIdx.x;
   for (int i = t; i < S; i += NT) {
     tw[i] = a.tw[i];
-    twr[i] = a.tw[(i % GR) * (i / GR)];
+    if constexpr (TWV) twr[i] = a.tw[((i >> 1) % GR) * ((i / (2 * GR)) * 2 + (i & 1))];  // [k/2][g][k%2]
+    else twr[i] = a.tw[(i % GR) * (i / GR)];
     twc[i] = a.tw[(i / RC) * (i % RC)];
   }
 
@@ -191,7 +217,17 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
   const T scale = TMEMP ? T(1) : a.scale;  // TMEM probe carries the 1/S
   const T inv1pl = T(1) / (T(1) + a.lam);
-  const int cx_ = t % CG, gc = t / CG;  // column-phase coordinates
+  // column-phase coordinates.  The warps form NSPLIT sets; set k owns columns
+  // [k CG/NSPLIT, (k+1) CG/NSPLIT) of every group, so a set exchanges only
+  // within itself (named barrier 1 + k) and the sets drift apart in time.
+  constexpr int SETT = NT / NSPLIT, SETC = CG / NSPLIT;  // threads, columns per set
+  const int cx_ = (t / SETT) * SETC + (t % SETT) % SETC;
+  const int gc = (t % SETT) / SETC;
+  auto col_sync = [&]() {
+    if constexpr (NSPLIT == 1) __syncthreads();
+    else if constexpr (SETT == 32) __syncwarp();
+    else named_bar(1 + t / SETT, SETT);
+  };
 
   // Prefetch registers: Gamma and amplitude of one column group.
   cx<T> pg[RC];
@@ -264,16 +300,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   do {              \
   } while (0)
 #endif
-  for (; i < iend; i = next_of(i)) {
-    const int f = frame_at(i);
-    const int64_t fbase = static_cast<int64_t>(f) * S * S;
-#ifdef PDD_BOUNDS
-    if (f < 0 || f >= a.nframes) {
-      printf("PDD_BOUNDS frame: cta %d i %d iend %d f %d\n", blockIdx.x, i, iend, f);
-      __trap();
-    }
-#endif
-    // ---------------- rows, forward
+  // ---------------- rows, forward (frame f): warp-local (each warp owns its rows)
+  auto fwd_rows = [&](int f) {
 #pragma unroll 1
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
@@ -293,9 +321,12 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
       dft<RR, false>(v);
 #pragma unroll
-      for (int k = 0; k < RR; ++k) {
-        const int k2 = k;
-        buf[y * P + k2 * GR + ((g + k2) & (GR - 1))] = (k == 0) ? v[k] : v[k] * twr[k * GR + g];
+      for (int k = 0; k < RR; k += 2) {
+        cx<T> t0, t1;
+        if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
+        else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
+        buf[y * P + k * GR + ((g + k) & (GR - 1))] = (k == 0) ? v[k] : v[k] * t0;
+        buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))] = v[k + 1] * t1;
       }
       __syncwarp();
 #pragma unroll
@@ -313,7 +344,32 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int k1 = 0; k1 < GR; ++k1) buf[y * P + k2 + RR * k1] = v[q * GR + k1];
       }
     }
+  };
+  constexpr bool FUSE = PDD_ROWFUSE && !FWD;
+  int pend_f = -1;  // FUSE: frame whose R-factor warp partials sit in red[]
+  if constexpr (FUSE) {
+    if (i < iend) fwd_rows(frame_at(i));
+  }
+  for (; i < iend; i = next_of(i)) {
+    const int f = frame_at(i);
+    const int64_t fbase = static_cast<int64_t>(f) * S * S;
+#ifdef PDD_BOUNDS
+    if (f < 0 || f >= a.nframes) {
+      printf("PDD_BOUNDS frame: cta %d i %d iend %d f %d\n", blockIdx.x, i, iend, f);
+      __trap();
+    }
+#endif
+    if constexpr (!FUSE) fwd_rows(f);
+    if constexpr (ACC) tmem_fence_before_sync();
     __syncthreads();
+    if constexpr (ACC) tmem_fence_after_sync();
+    if constexpr (FUSE) {
+      if (pend_f >= 0 && a.rf_part && t == 0) {
+        double s = 0.0;
+        for (int w = 0; w < NT / 32; ++w) s += red[w];
+        a.rf_part[pend_f] = s;
+      }
+    }
     PDD_TICK(0);
 
     // ---------------- column groups: forward, prox, inverse
@@ -326,8 +382,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
       dft<RC, false>(w);
 #pragma unroll
-      for (int k = 0; k < RC; ++k) buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * twc[gc * RC + k];
-      __syncthreads();
+      for (int k = 0; k < RC; k += 2) {
+        cx<T> t0, t1;
+        if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
+        else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
+        buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * t0;
+        buf[((k + 1) * GC + gc) * P + x] = w[k + 1] * t1;
+      }
+      col_sync();
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
         const int k2 = gc + GC * q;
@@ -390,11 +452,15 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int gp = 0; gp < GC; ++gp) buf[(k2 * GC + gp) * P + x] = w[q * GC + gp];
       }
-      __syncthreads();
+      col_sync();
 #pragma unroll
-      for (int k = 0; k < RC; ++k) {
-        const cx<T> v = buf[(k * GC + gc) * P + x];
-        w[k] = (k == 0) ? v : mul_conj(v, twc[gc * RC + k]);
+      for (int k = 0; k < RC; k += 2) {
+        cx<T> t0, t1;
+        if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
+        else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
+        const cx<T> v0 = buf[(k * GC + gc) * P + x], v1 = buf[((k + 1) * GC + gc) * P + x];
+        w[k] = (k == 0) ? v0 : mul_conj(v0, t0);
+        w[k + 1] = mul_conj(v1, t1);
       }
       dft<RC, true>(w);
 #pragma unroll
@@ -443,9 +509,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < RR; ++k) {
-        const cx<T> b = buf[y * P + k * GR + ((g + k) & (GR - 1))];
-        v[k] = (k == 0) ? b : mul_conj(b, twr[k * GR + g]);
+      for (int k = 0; k < RR; k += 2) {
+        cx<T> t0, t1;
+        if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
+        else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
+        const cx<T> b0 = buf[y * P + k * GR + ((g + k) & (GR - 1))];
+        const cx<T> b1 = buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))];
+        v[k] = (k == 0) ? b0 : mul_conj(b0, t0);
+        v[k + 1] = mul_conj(b1, t1);
       }
       if (tma_rows && fn >= 0) {
         __syncwarp();             // this warp's rows are consumed
@@ -496,15 +567,31 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int o = 16; o > 0; o >>= 1) rf += __shfl_down_sync(0xffffffffu, rf, o);
       if ((t & 31) == 0) red[t >> 5] = rf;
     }
-    if constexpr (ACC) tmem_fence_before_sync();  // accumulator rows change warps between frames
-    __syncthreads();  // also: rows of the next frame overwrite buf
-    if constexpr (ACC) tmem_fence_after_sync();
-    if (a.rf_part && t == 0) {
-      double s = 0.0;
-      for (int w = 0; w < NT / 32; ++w) s += red[w];
-      a.rf_part[f] = s;
+    if constexpr (FUSE) {
+      // the next frame's forward rows follow at once: a warp touches only its
+      // own rows of buf, and the accumulator rows that change warps between
+      // frames are ordered by the two barriers of the next frame
+      pend_f = f;
+      if (fn >= 0) fwd_rows(fn);
+    } else {
+      if constexpr (ACC) tmem_fence_before_sync();  // accumulator rows change warps between frames
+      __syncthreads();  // also: rows of the next frame overwrite buf
+      if constexpr (ACC) tmem_fence_after_sync();
+      if (a.rf_part && t == 0) {
+        double s = 0.0;
+        for (int w = 0; w < NT / 32; ++w) s += red[w];
+        a.rf_part[f] = s;
+      }
     }
     PDD_TICK(3);
+  }
+  if constexpr (FUSE) {
+    __syncthreads();
+    if (pend_f >= 0 && a.rf_part && t == 0) {
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += red[w];
+      a.rf_part[pend_f] = s;
+    }
   }
 #ifdef PDD_CANARY
   __syncthreads();

@@ -222,10 +222,6 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sm) {
 }
 
 
-#ifndef PDD_GPRED
-#define PDD_GPRED 0  // gather: predicated PTX loads instead of branches around the loads
-#endif
-
 // Streaming (evict-first) load of a complex value: back-projection tiles are
 // read exactly once.
 template <typename T>
@@ -322,16 +318,7 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
         const bool ok = static_cast<unsigned>(cc) < static_cast<unsigned>(S) &&
                         static_cast<unsigned>(rr) < static_cast<unsigned>(s_h[k]);
         L q{};
-        const L* src = reinterpret_cast<const L*>(a.bp + s_base[k] + static_cast<int64_t>(rr) * S + cc + v);
-        if constexpr (PDD_GPRED && std::is_same_v<L, float4>) {
-          // one predicated streaming load: no branch or reconvergence around it
-          asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "@p ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%5];\n\t}"
-              : "+f"(q.x), "+f"(q.y), "+f"(q.z), "+f"(q.w)
-              : "r"(static_cast<int>(ok)), "l"(src));
-        } else {
-          if (ok) q = __ldcs(src);
-        }
+        if (ok) q = __ldcs(reinterpret_cast<const L*>(a.bp + s_base[k] + static_cast<int64_t>(rr) * S + cc + v));
         return q;
       };
       auto add = [&](int i, int v, const L& q) {

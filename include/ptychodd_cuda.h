@@ -237,6 +237,13 @@ PDD_API int pdd_estimate_support_mask(const double* probe_guess, int64_t side, d
 /* ---- pinned host memory for end-to-end staging ----------------------------- */
 PDD_API int pdd_host_alloc(void** p, int64_t bytes);
 PDD_API int pdd_host_free(void* p);
+/* Reserve the library's page-locked download staging buffer now (idempotent).
+ * Large results (sub-solutions, merged image, state) are copied out through it
+ * by several host threads; the Python front end calls this on its helper thread
+ * while the device loop of run() executes, so the first download does not pay
+ * for the allocation.  No reference counterpart (reference results are host
+ * values already). */
+PDD_API int pdd_host_stage_reserve(void);
 
 #ifdef __cplusplus
 }

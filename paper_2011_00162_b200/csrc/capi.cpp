@@ -695,6 +695,9 @@ int pdd_host_alloc(void** p, int64_t bytes) {
     pdd::cuda_check(cudaMallocHost(p, static_cast<size_t>(bytes)), "cudaMallocHost");
   });
 }
+int pdd_host_stage_reserve(void) {
+  return guard([&] { pdd::host_stage_reserve(); });
+}
 int pdd_host_free(void* p) {
   return guard([&] {
     if (p) pdd::cuda_check(cudaFreeHost(p), "cudaFreeHost");

@@ -10,6 +10,9 @@
 #include <complex>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "device.hpp"
@@ -53,12 +56,103 @@ std::vector<cx<T>> download_cx(const void* dev, int64_t n, cudaStream_t st) {
   return h;
 }
 
-// Device complex<T> -> host complex128 without a host-side conversion loop
-// (float data is widened on the device in chunks, then copied straight into
-// the caller's buffer).
+// PDD_TIMING=1: setup phase timings on stderr (developer aid).
+struct SetupTimer {
+  bool on = std::getenv("PDD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pdd] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
+// Large device -> host result copies (the e2e downloads: sub-solutions, merged
+// image, state).  A plain cudaMemcpy into pageable memory runs at ~17 GB/s on
+// the B200 hosts (the driver bounces through its own staging buffer on one
+// thread).  Here W host threads each own a slice of a page-locked staging
+// buffer and a stream: a thread DMAs its next chunk of T-precision data (at
+// the full ~57 GB/s shared by all threads), then widens it to complex128 into
+// the caller's buffer while the other threads' DMAs proceed.  float data thus
+// crosses PCIe at half the bytes and is widened on the host (exact).
+struct HostStage {
+  static constexpr size_t kBytes = size_t(32) << 20;  // total page-locked staging
+  std::mutex mu;
+  void* buf = nullptr;
+  int workers = 0;  // the buffer lives for the process (no CUDA calls in static destructors)
+  void reserve_locked() {
+    if (buf) return;
+    PDD_CUDA(cudaHostAlloc(&buf, kBytes, cudaHostAllocPortable));
+    workers = static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 2u, 16u));
+  }
+  void reserve() {
+    std::lock_guard<std::mutex> lock(mu);
+    reserve_locked();
+  }
+  static HostStage& get() {
+    static HostStage s;
+    return s;
+  }
+};
+
+template <typename T>
+void download_c128_staged(const cx<T>* dev, int64_t n, double* out, cudaStream_t st) {
+  PDD_CUDA(cudaStreamSynchronize(st));  // the producer's work is complete
+  SetupTimer tm;
+  int device = 0;
+  PDD_CUDA(cudaGetDevice(&device));
+  HostStage& hs = HostStage::get();
+  std::lock_guard<std::mutex> lock(hs.mu);
+  hs.reserve_locked();
+  tm.mark("staged: lock+alloc");
+  const int W = hs.workers;
+  const int64_t chunk = static_cast<int64_t>(HostStage::kBytes / W / sizeof(cx<T>));
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  std::vector<cudaError_t> err(W, cudaSuccess);
+  std::vector<std::thread> th;
+  for (int k = 0; k < W; ++k)
+    th.emplace_back([&, k] {
+      cudaError_t e = cudaSetDevice(device);
+      cudaStream_t s = nullptr;
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      cx<T>* stage = reinterpret_cast<cx<T>*>(static_cast<char*>(hs.buf) + HostStage::kBytes / W * k);
+      for (int64_t c = k; c < nchunks && e == cudaSuccess; c += W) {
+        const int64_t o = c * chunk, m = std::min(chunk, n - o);
+        e = cudaMemcpyAsync(stage, dev + o, sizeof(cx<T>) * m, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) break;
+        if constexpr (sizeof(T) == sizeof(double)) {
+          std::memcpy(out + 2 * o, stage, sizeof(cx<T>) * m);
+        } else {
+          double* q = out + 2 * o;
+          for (int64_t i = 0; i < m; ++i) {
+            q[2 * i] = static_cast<double>(stage[i].x);
+            q[2 * i + 1] = static_cast<double>(stage[i].y);
+          }
+        }
+      }
+      if (s) cudaStreamDestroy(s);
+      err[k] = e;
+    });
+  for (auto& x : th) x.join();
+  tm.mark("staged: copy");
+  for (cudaError_t e : err) PDD_CUDA(e);
+}
+
+// Device complex<T> -> host complex128.  Large copies go through the staged
+// multi-threaded path above; small ones widen on the device and copy directly.
 template <typename T>
 void download_c128(const void* dev, int64_t n, double* out, cudaStream_t st) {
   if (n <= 0) return;
+  static const bool staged = [] {
+    const char* e = std::getenv("PDD_STAGED_D2H");
+    return !(e && e[0] == '0');
+  }();
+  if (staged && n >= (int64_t(1) << 20)) {
+    download_c128_staged<T>(static_cast<const cx<T>*>(dev), n, out, st);
+    return;
+  }
   if constexpr (sizeof(T) == sizeof(double)) {
     PDD_CUDA(cudaMemcpyAsync(out, dev, sizeof(cx<double>) * n, cudaMemcpyDeviceToHost, st));
   } else {
@@ -82,17 +176,6 @@ void upload_cx(void* dev, const double* src, int64_t n, cudaStream_t st) {
   PDD_CUDA(cudaStreamSynchronize(st));
 }
 
-// PDD_TIMING=1: setup phase timings on stderr (developer aid).
-struct SetupTimer {
-  bool on = std::getenv("PDD_TIMING") != nullptr;
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  void mark(const char* what) {
-    if (!on) return;
-    const auto t = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[pdd] %-24s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
-    t0 = t;
-  }
-};
 
 template <typename T>
 struct RankData {
@@ -392,7 +475,11 @@ struct RankData {
   }
 
   // merge (ddplan.cpp:104-121) of the device sub-solutions into a host image.
-  void merge_to_host(const Plan& plan, const cx<T>* u, double* out) {
+  // scratch: optional device buffer free at this point (>= H*W complex128),
+  // e.g. the nonblind back-projection scratch -- a fresh 1 GB cudaMalloc here
+  // cost 1-90 ms (and ~0.4 s on a process's first large allocation).
+  void merge_to_host(const Plan& plan, const cx<T>* u, double* out, void* scratch = nullptr,
+                     size_t scratch_bytes = 0) {
     if (L.nls() != plan.D) throw InvalidArgument("merge: this rank does not own every subdomain");
     cudaStream_t s = st();
     std::vector<int64_t> rect;
@@ -404,11 +491,17 @@ struct RankData {
     }
     DevMem drect = upload(rect, s);
     const int64_t n = plan.g.H * plan.g.W;
-    DevMem img(sizeof(cx<double>) * n);
-    PDD_CUDA(launch_merge<T>(u, drect.as<int64_t>(), sub_off.as<int64_t>(), plan.D, plan.g.H, plan.g.W,
-                             img.as<cx<double>>(), s));
-    PDD_CUDA(cudaMemcpyAsync(out, img.get(), sizeof(cx<double>) * n, cudaMemcpyDeviceToHost, s));
-    PDD_CUDA(cudaStreamSynchronize(s));
+    SetupTimer tm;
+    DevMem img;
+    cx<double>* dst = static_cast<cx<double>*>(scratch);
+    if (!dst || scratch_bytes < sizeof(cx<double>) * n) {
+      img.alloc(sizeof(cx<double>) * n);
+      dst = img.as<cx<double>>();
+    }
+    tm.mark("merge: alloc");
+    PDD_CUDA(launch_merge<T>(u, drect.as<int64_t>(), sub_off.as<int64_t>(), plan.D, plan.g.H, plan.g.W, dst, s));
+    download_c128<double>(dst, n, out, s);
+    tm.mark("merge: kernel+download");
   }
 
   void reset_ctl(int iter, int max_iters, int rule, double tol_rf, double tol_re) {

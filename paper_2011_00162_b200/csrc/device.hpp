@@ -16,6 +16,9 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define PDD_CUDA(call) ::pdd::cuda_check((call), #call)
 
+// Page-locked download staging (common.cuh HostStage), reserved ahead of use.
+void host_stage_reserve();
+
 // Untyped device allocation.  Freed on destruction.
 class DevMem {
  public:

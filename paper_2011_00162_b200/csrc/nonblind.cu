@@ -21,6 +21,9 @@
 
 namespace pdd {
 
+void host_stage_reserve() { HostStage::get().reserve(); }
+
+
 void NonblindConfig::validate() const {  // solver.cpp:24-31
   if (!(epsilon > 0.0 && epsilon < 1.0)) throw InvalidArgument("stagm: epsilon must lie in (0,1)");
   if (eta <= 0.0 || r <= 0.0) throw InvalidArgument("NonblindConfig: eta, r must be > 0");
@@ -500,7 +503,9 @@ class Nonblind final : public NonblindGpu {
     download_c128<T>(bp_.get(), R.L.nfr * R.SS(), au, R.st());
   }
 
-  void merged(double* out) override { R.merge_to_host(plan_, U(iter_), out); }
+  void merged(double* out) override {  // bp_ is per-iteration scratch
+    R.merge_to_host(plan_, U(iter_), out, bp_.get(), bp_.bytes());
+  }
   void sync() override { R.stream.sync(); }
   int64_t kernel_launches_per_iteration() const override { return 10; }
 

@@ -496,17 +496,21 @@ class _Prefault(threading.Thread):
     """Allocates and maps the host result buffers on a helper thread while the
     device loop runs (the C-ABI call releases the GIL).  (Page-locking them
     instead costs more than it saves: cudaMallocHost of 2 GB takes ~0.9 s and
-    stalls the device loop.)"""
+    stalls the device loop.)  It also reserves the library's small page-locked
+    staging buffer through which the results are downloaded."""
 
     def __init__(self, *shapes):
         super().__init__(daemon=True)
-        self.shapes, self.out = shapes, None
+        self.shapes, self.out, self.rc = shapes, None, 0
 
     def run(self):
+        # the library's page-locked download staging (a no-op after the first call)
+        self.rc = L.lib().pdd_host_stage_reserve()
         self.out = [_prefaulted(sh) for sh in self.shapes]
 
     def result(self):
         self.join()
+        check(self.rc)
         return self.out
 
 

@@ -344,11 +344,13 @@ class Blind final : public BlindGpu {
 
   void ensure_graphs() {
     if (full_[0].ready()) return;
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < 2; ++p) {
       full_[p].capture(R.st(), [&] {
         enqueue_iteration(p, false);
         enqueue_iteration(1 - p, false);
       });
+      one_[p].capture(R.st(), [&] { enqueue_iteration(p, false); });
+    }
     tail_.capture(R.st(), [&] { enqueue_tail(); });
   }
 
@@ -380,7 +382,10 @@ class Blind final : public BlindGpu {
     while (launched < max_total) {
       const int batch = std::min(kPoll, (max_total - launched + 1) / 2);
       for (int b = 0; b < batch; ++b) {
-        full_[parity].launch(s);
+        if (!tail && launched + 2 * b + 1 == max_total)
+          one_[parity].launch(s);  // odd count, no trailing R-factor pass (nonblind.cu drive)
+        else
+          full_[parity].launch(s);
         cudaEvent_t e;
         PDD_CUDA(cudaEventCreate(&e));
         PDD_CUDA(cudaEventRecord(e, s));
@@ -567,7 +572,7 @@ class Blind final : public BlindGpu {
   DevMem one_off_, one_pitch_, chunk_f0_, chunk_f1_, chunk_beg_, num_part_, den_part_;
   int nchunks_ = 0;
   std::vector<double> w0_, mask_h_;
-  Graph full_[2], tail_;
+  Graph full_[2], one_[2], tail_;
   int64_t iter_ = 0;
   bool z_valid_ = false;
 };

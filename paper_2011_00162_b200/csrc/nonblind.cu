@@ -226,6 +226,7 @@ class Nonblind final : public NonblindGpu {
         enqueue_iteration(1 - p, false);
       });
       tail_[p].capture(R.st(), [&] { enqueue_tail(p); });
+      one_[p].capture(R.st(), [&] { enqueue_iteration(p, false); });
     }
   }
 
@@ -259,7 +260,14 @@ class Nonblind final : public NonblindGpu {
     while (launched < max_total) {
       const int batch = std::min(kPoll, (max_total - launched + 1) / 2);
       for (int b = 0; b < batch; ++b) {
-        full_[parity].launch(s);  // parity is preserved across a 2-iteration graph
+        if (!tail && launched + 2 * b + 1 == max_total) {
+          // odd count without the trailing R-factor pass: a one-iteration graph
+          // (the second half of a pair would run the final iterate's frame
+          // pass, i.e. the R-factor pass this call leaves out)
+          one_[parity].launch(s);
+        } else {
+          full_[parity].launch(s);  // parity is preserved across a 2-iteration graph
+        }
         cudaEvent_t e;
         PDD_CUDA(cudaEventCreate(&e));
         PDD_CUDA(cudaEventRecord(e, s));
@@ -517,7 +525,7 @@ class Nonblind final : public NonblindGpu {
   DevMem probe_, probe64_, gamma_[2], bp_, u_[2], v_[2], lam_[2], s_, denom_, z_;
   DevMem lag_fr_, lag_pr_, lag_glob_;
   std::vector<double> last_lag_;
-  Graph full_[2], tail_[2];
+  Graph full_[2], tail_[2], one_[2];
   int64_t iter_ = 0;
   bool z_valid_ = false;
 };

@@ -257,3 +257,30 @@ def test_singular_density_raises_runtime_error():
         P.NonblindSolver(plan, f, dark, P.NonblindConfig(r=0.0))
     with pytest.raises(ValueError):
         P.NonblindSolver(plan, f, dark, P.NonblindConfig(), np.zeros((8, 8)))
+
+
+@pytest.mark.parametrize("n", [1, 3, 4])
+def test_timed_iterations_run_exactly_n(n):
+    """The benchmark's pdd_nonblind_iterate_timed(n) runs exactly n iterations
+    (odd n: a one-iteration graph ends the loop, no extra frame pass) and
+    leaves the iterate bit-identical to pdd_nonblind_iterate(n)."""
+    import ctypes as C
+    from paper_2011_00162_b200 import _lib as L
+
+    probe, f, _, plan = small_problem(N=512, s=128, step=32, D=2, peak=1e4)
+    out = []
+    for timed in (False, True):
+        gs = P.NonblindSolver(plan, fp32_intensity(f), probe, P.NonblindConfig(max_iters=16, tol_rf=1e-300),
+                              dtype="f32")
+        if timed:
+            ms = C.c_double()
+            L.check(L.lib().pdd_nonblind_iterate_timed(gs._h, C.c_int32(n), C.byref(ms)))
+            assert ms.value > 0.0
+        else:
+            gs.iterate(n)
+        u = np.zeros(gs._lay.image_elems, np.complex128)
+        it = C.c_int64()
+        L.check(L.lib().pdd_nonblind_get_state(gs._h, L.ptr(u), None, None, None, None, C.byref(it)))
+        assert it.value == n
+        out.append(u)
+    assert np.array_equal(out[0], out[1])

@@ -284,3 +284,44 @@ def test_timed_iterations_run_exactly_n(n):
         assert it.value == n
         out.append(u)
     assert np.array_equal(out[0], out[1])
+
+
+_DL_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2011_00162_b200 as P
+from paper_2011_00162_b200 import sim
+from oracle import od2p as O
+N, s, step = 1024, 64, 32
+probe = sim.make_probe(s, s / 4)
+obj = sim.make_object(N, 4.0, 1, 2)
+f = O.intensity(O.forward(probe, obj, O.make_raster_scan(N, N, s, step)))
+plan = P.plan_stripes(P.make_raster_scan(N, N, s, step), 2, "rows")
+gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=3, tol_rf=1e-300), dtype="f32")
+res = gs.run()
+st = gs._get_state()
+np.savez(sys.argv[2], merged=res.merged, u=np.concatenate([u.ravel() for u in res.sub_solutions]),
+         gamma=np.concatenate([g.ravel() for g in st.gamma]))
+"""
+
+
+def test_staged_downloads_are_exact(tmp_path):
+    """Result downloads through the page-locked staging ring (host-side
+    widening, multi-threaded) equal the plain device-widened copies bit for
+    bit: merged image (> 1M pixels), sub-solutions and Gamma."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for staged in ("1", "0"):
+        path = tmp_path / f"dl{staged}.npz"
+        env = dict(os.environ, PDD_STAGED_D2H=staged)
+        subprocess.run([sys.executable, "-c", _DL_SCRIPT, root, str(path)], check=True, env=env, cwd=root,
+                       timeout=600)
+        out[staged] = np.load(path)
+    for k in ("merged", "u", "gamma"):
+        assert out["1"][k].size >= (1 << 20) or k == "u"
+        assert np.array_equal(out["1"][k], out["0"][k]), k

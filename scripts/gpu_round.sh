@@ -10,7 +10,7 @@ bash scripts/gpu_bench.sh
 if [ "${NCU:-1}" = 1 ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_stream -c 1 \
     -o gpurun_out/sweep_$TAG -f python scripts/prof_frame.py 4 1 > gpurun_out/ncu_sweep_$TAG.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:gather_kernelIf -c 1 \
     -o gpurun_out/gather_$TAG -f python scripts/prof_frame.py 4 1 > gpurun_out/ncu_gather_$TAG.log 2>&1
   tail -n 1 gpurun_out/ncu_sweep_$TAG.log gpurun_out/ncu_gather_$TAG.log
 fi

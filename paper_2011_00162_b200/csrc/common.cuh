@@ -5,6 +5,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <chrono>
 #include <complex>
@@ -90,6 +91,21 @@ struct HostStage {
     std::lock_guard<std::mutex> lock(mu);
     reserve_locked();
   }
+  // At solver construction: the first page-locked allocation of a process
+  // takes tens of ms, so it runs on a helper thread while the amplitudes
+  // upload and the device loop execute (errors resurface at the first use).
+  void reserve_async(int device) {
+    if (started.exchange(true)) return;
+    std::thread([this, device] {
+      try {
+        PDD_CUDA(cudaSetDevice(device));
+        reserve();
+      } catch (...) {
+        cudaGetLastError();
+      }
+    }).detach();
+  }
+  std::atomic<bool> started{false};
   static HostStage& get() {
     static HostStage s;
     return s;
@@ -212,6 +228,7 @@ struct RankData {
     comm = c;
     const int rank = c ? c->rank() : 0, world = c ? c->world() : 1;
     SetupTimer tm;
+    HostStage::get().reserve_async(dev);  // result-download staging, off the critical path
     L = Layout::build(plan, rank, world, sizeof(T) == 4, piece_len);
     tm.mark("layout");
     S = L.S;

@@ -121,6 +121,20 @@ def bcast_obj(dist, obj, rank):
     return lst[0]
 
 
+def fresh_nccl_id(dist, rank, world):
+    """A new NCCL unique id from rank 0 for each communicator (an id's bootstrap
+    root serves a single ncclCommInitRank round), or None on one GPU."""
+    if world <= 1:
+        return None
+    import ctypes as C
+
+    from paper_2011_00162_b200 import _lib as L
+
+    buf = C.create_string_buffer(128)
+    if rank == 0:
+        L.check(L.lib().pdd_nccl_unique_id(buf))
+    return bcast_obj(dist, bytes(buf.raw) if rank == 0 else None, rank)
+
 def allmax(dist, x: float) -> float:
     if dist is None:
         return x
@@ -260,14 +274,7 @@ def main():
     inp = sim.make_inputs(cfg, device=True)
     plan, probe, amp = inp["plan"], inp["probe"], inp["amplitudes_dev"]
     J, s = plan.geometry.frame_count(), cfg.s
-    nccl_id = None
-    if world > 1:
-        import ctypes as C
-
-        buf = C.create_string_buffer(128)
-        if rank == 0:
-            L.check(L.lib().pdd_nccl_unique_id(buf))
-        nccl_id = bcast_obj(dist, bytes(buf.raw) if rank == 0 else None, rank)
+    nccl_id = fresh_nccl_id(dist, rank, world)
     ncfg = P.NonblindConfig(max_iters=max(cfg.iterations, args.steps + args.warmup + 8), tol_rf=1e-300)
     solver = P.NonblindSolver(plan, None, probe, ncfg, amplitudes=amp, dtype=cfg.dtype, device=local, rank=rank,
                               world=world, nccl_id=nccl_id)
@@ -337,6 +344,7 @@ def main():
         amp_np = host.numpy()
         del amp
         torch.cuda.empty_cache()
+        nccl_id = fresh_nccl_id(dist, rank, world)  # a unique id bootstraps one communicator only
         if dist:
             dist.barrier()
         n_e2e = cfg.iterations
@@ -382,12 +390,7 @@ def bench_blind(args, cfg, base, rank, world, local, dist):
     plan, amp = inp["plan"], inp["amplitudes_dev"]
     J, s = plan.geometry.frame_count(), cfg.s
     w0 = inp.get("w0")
-    nccl_id = None
-    if world > 1:
-        buf = C.create_string_buffer(128)
-        if rank == 0:
-            L.check(L.lib().pdd_nccl_unique_id(buf))
-        nccl_id = bcast_obj(dist, bytes(buf.raw) if rank == 0 else None, rank)
+    nccl_id = fresh_nccl_id(dist, rank, world)
     bcfg = P.BlindConfig(max_iters=max(cfg.iterations, args.steps + args.warmup + 8), tol_rf=1e-300, **cfg.solver)
     solver = P.BlindSolver(plan, None, bcfg, amplitudes=amp, dtype=cfg.dtype, device=local, rank=rank, world=world,
                            nccl_id=nccl_id)
@@ -440,6 +443,7 @@ def bench_blind(args, cfg, base, rank, world, local, dist):
         amp_np = host.numpy()
         del amp
         torch.cuda.empty_cache()
+        nccl_id = fresh_nccl_id(dist, rank, world)  # a unique id bootstraps one communicator only
         if dist:
             dist.barrier()
         ecfg = P.BlindConfig(max_iters=cfg.iterations, tol_rf=1e-300, **cfg.solver)

@@ -163,3 +163,33 @@ def test_two_rank_iteration_equals_single_process(kind):
         assert abs(rrf - rf) < 1e-12 * rf and abs(rre - re) < 1e-12 * re
     assert seen_u == set(range(oplan.D))
     assert len(seen_l) == 2 * len(oplan.overlaps)
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, ROOT)
+    import bench
+
+    d = bench.init_dist(world)
+    try:
+        q.put((rank, bench.fresh_nccl_id(d, rank, world), bench.fresh_nccl_id(d, rank, world)))
+    finally:
+        d.destroy_process_group()
+
+
+def test_bench_draws_a_fresh_nccl_id_per_communicator():
+    """bench.py builds two solvers per rank (timed loop, then e2e); an NCCL
+    unique id bootstraps one communicator only, so each gets its own id, the
+    same on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, a0, b0), (_, a1, b1) = res
+    assert len(a0) == 128 and a0 == a1 and b0 == b1 and a0 != b0

@@ -85,7 +85,9 @@ struct HostStage {
   void reserve_locked() {
     if (buf) return;
     PDD_CUDA(cudaHostAlloc(&buf, kBytes, cudaHostAllocPortable));
-    workers = static_cast<int>(std::clamp(std::thread::hardware_concurrency(), 2u, 16u));
+    // half the host threads (at most 8): the copy saturates at ~8 threads, and
+    // leaving cores free keeps a descheduled worker from stalling the drain
+    workers = static_cast<int>(std::clamp(std::thread::hardware_concurrency() / 2, 2u, 8u));
   }
   void reserve() {
     std::lock_guard<std::mutex> lock(mu);
@@ -127,13 +129,14 @@ void download_c128_staged(const cx<T>* dev, int64_t n, double* out, cudaStream_t
   const int64_t nchunks = (n + chunk - 1) / chunk;
   std::vector<cudaError_t> err(W, cudaSuccess);
   std::vector<std::thread> th;
+  std::atomic<int64_t> next{0};  // chunks handed out on demand: a slow worker takes fewer
   for (int k = 0; k < W; ++k)
     th.emplace_back([&, k] {
       cudaError_t e = cudaSetDevice(device);
       cudaStream_t s = nullptr;
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
       cx<T>* stage = reinterpret_cast<cx<T>*>(static_cast<char*>(hs.buf) + HostStage::kBytes / W * k);
-      for (int64_t c = k; c < nchunks && e == cudaSuccess; c += W) {
+      for (int64_t c = next.fetch_add(1); c < nchunks && e == cudaSuccess; c = next.fetch_add(1)) {
         const int64_t o = c * chunk, m = std::min(chunk, n - o);
         e = cudaMemcpyAsync(stage, dev + o, sizeof(cx<T>) * m, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -124,16 +124,9 @@ def bcast_obj(dist, obj, rank):
 def fresh_nccl_id(dist, rank, world):
     """A new NCCL unique id from rank 0 for each communicator (an id's bootstrap
     root serves a single ncclCommInitRank round), or None on one GPU."""
-    if world <= 1:
-        return None
-    import ctypes as C
+    from paper_2011_00162_b200 import dist as pdist
 
-    from paper_2011_00162_b200 import _lib as L
-
-    buf = C.create_string_buffer(128)
-    if rank == 0:
-        L.check(L.lib().pdd_nccl_unique_id(buf))
-    return bcast_obj(dist, bytes(buf.raw) if rank == 0 else None, rank)
+    return pdist.new_nccl_id(pdist.DistContext(rank, world, 0, None, dist))
 
 def allmax(dist, x: float) -> float:
     if dist is None:

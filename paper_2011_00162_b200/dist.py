@@ -37,15 +37,25 @@ def init(backend: str = "gloo", need_nccl_id: bool = True) -> DistContext:
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     if not dist.is_initialized():
         dist.init_process_group(backend)
-    nid = None
+    ctx = DistContext(rank, world, local, None, dist)
     if need_nccl_id:
-        buf = C.create_string_buffer(128)
-        if rank == 0:
-            L.check(L.lib().pdd_nccl_unique_id(buf))
-        lst = [bytes(buf.raw) if rank == 0 else None]
-        dist.broadcast_object_list(lst, src=0)
-        nid = lst[0]
-    return DistContext(rank, world, local, nid, dist)
+        ctx.nccl_id = new_nccl_id(ctx)
+    return ctx
+
+
+def new_nccl_id(ctx: DistContext) -> Optional[bytes]:
+    """A fresh NCCL unique id, drawn on rank 0 and broadcast (collective over
+    the process group).  An id bootstraps ONE communicator: every solver after
+    the first needs a new one (reusing an id leaves ncclCommInitRank waiting
+    for a bootstrap root that has already exited)."""
+    if ctx.world <= 1:
+        return None
+    buf = C.create_string_buffer(128)
+    if ctx.rank == 0:
+        L.check(L.lib().pdd_nccl_unique_id(buf))
+    lst = [bytes(buf.raw) if ctx.rank == 0 else None]
+    ctx.dist.broadcast_object_list(lst, src=0)
+    return lst[0]
 
 
 @dataclass

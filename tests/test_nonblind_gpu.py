@@ -325,3 +325,22 @@ def test_staged_downloads_are_exact(tmp_path):
     for k in ("merged", "u", "gamma"):
         assert out["1"][k].size >= (1 << 20) or k == "u"
         assert np.array_equal(out["1"][k], out["0"][k]), k
+
+
+def test_repeated_solves_reuse_pooled_device_memory():
+    """DevMem draws from the device's stream-ordered pool and keeps freed
+    memory mapped: building and running the same solver again does not grow
+    the device footprint (no leak, no second mapping)."""
+    import torch
+
+    probe, f, _, plan = small_problem(N=512, s=128, step=32, D=2, peak=1e4)
+    f = fp32_intensity(f)
+    free = []
+    merged = []
+    for _ in range(3):
+        res = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=3, tol_rf=1e-300), dtype="f32").run()
+        merged.append(res.merged)
+        torch.cuda.synchronize()
+        free.append(torch.cuda.mem_get_info()[0])
+    assert free[2] >= free[1] - (64 << 20), free
+    assert np.array_equal(merged[0], merged[2])

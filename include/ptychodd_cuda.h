@@ -135,7 +135,11 @@ typedef struct pdd_nonblind pdd_nonblind;
 
 /* NonblindSolver(plan, frames, probe, config, pin_ones): data [J][s][s] of data_kind in
  * global scan order (host memory unless data_on_device); probe [s][s] c128; pin_ones
- * [H][W] f64 or NULL.  device = CUDA ordinal. */
+ * [H][W] f64 or NULL.  device = CUDA ordinal.
+ * Ordering contract for data_on_device: the solver copies the data on its own
+ * stream, which is not ordered after the caller's streams -- every write to the
+ * buffer must be complete (e.g. cudaStreamSynchronize of the producing stream)
+ * before the call.  The buffer may be reused or freed when the call returns. */
 PDD_API int pdd_nonblind_create(const pdd_plan* plan, const void* data, int32_t data_kind, int32_t data_on_device,
                         const double* probe, const pdd_nonblind_config* cfg, const double* pin_ones, int32_t dtype,
                         int32_t device, pdd_nonblind** out);
@@ -146,6 +150,22 @@ PDD_API int pdd_nonblind_create_rank(const pdd_plan* plan, const void* data, int
                              const double* probe, const pdd_nonblind_config* cfg, const double* pin_ones,
                              int32_t dtype, int32_t device, int32_t rank, int32_t world, const void* nccl_id,
                              pdd_nonblind** out);
+/* One handle driving n_devices ranks of this process -- the reference's worker
+ * pool (NonblindConfig::threads, solver.hpp:25; WorkerPool, parallel.hpp:14-90)
+ * mapped onto GPUs: rank r on devices[r] owns subdomains d with
+ * floor(d*n_devices/D) == r (n_devices <= D), each rank on its own host thread,
+ * stream and CUDA graphs; NCCL between distinct devices, the in-process host
+ * transport when a device repeats (several ranks on one GPU: the multi-rank
+ * code path without NCCL).  Iterates are bit-identical for every n_devices at
+ * fixed D.  State arrays use the single-handle layout above. */
+PDD_API int pdd_nonblind_create_multi(const pdd_plan* plan, const void* data, int32_t data_kind,
+                                      int32_t data_on_device, const double* probe, const pdd_nonblind_config* cfg,
+                                      const double* pin_ones, int32_t dtype, const int32_t* devices,
+                                      int32_t n_devices, pdd_nonblind** out);
+/* A 128-byte id for the in-process host transport, usable in place of an NCCL
+ * id by pdd_*_create_rank when the ranks are threads of one process (tests of
+ * the rank-sharded path on one device).  No reference counterpart. */
+PDD_API int pdd_host_transport_id(void* out128);
 /* Sizes of the state arrays held by this handle (complex element counts). */
 typedef struct {
   int32_t n_local_sub, n_local_pairs;
@@ -161,6 +181,17 @@ PDD_API int pdd_nonblind_step(pdd_nonblind* h, int32_t store_z);       /* solver
 /* run() (solver.cpp:216-267) from a fresh init_state.  records: [max_iters][3] (rf, re, t_ms);
  * returns PDD_DIVERGENCE with *diverged_at set if RF/RE became non-finite. */
 PDD_API int pdd_nonblind_run(pdd_nonblind* h, int64_t* iterations, double* records, int64_t* diverged_at);
+/* run() with the reference's per-iteration callback (solver.hpp:88
+ * on_iteration): cb(iteration, rf, re, t_ms, lagrangian, user) is called on the
+ * calling thread while the device loop runs -- in order, once per iteration,
+ * at most one poll window (16 iterations) behind the device, never for
+ * iterations a stop rule rolls back.  lagrangian is NaN unless
+ * record_lagrangian.  cb may be NULL (== pdd_nonblind_run).  It runs on the
+ * thread that drives the device loop: the caller's, or rank 0's worker thread
+ * for pdd_nonblind_create_multi handles. */
+typedef void (*pdd_record_cb)(int64_t iteration, double rf, double re, double t_ms, double lagrangian, void* user);
+PDD_API int pdd_nonblind_run_cb(pdd_nonblind* h, pdd_record_cb cb, void* user, int64_t* iterations, double* records,
+                                int64_t* diverged_at);
 /* Exactly n iterations from the current state (no stop rule, no host round trip). */
 PDD_API int pdd_nonblind_iterate(pdd_nonblind* h, int32_t n);
 /* Same, reporting the device time of the n iterations (CUDA events on the solver stream). */
@@ -204,12 +235,19 @@ PDD_API int pdd_blind_create_rank(const pdd_plan* plan, const void* data, int32_
                           const pdd_blind_config* cfg, const double* support_mask, const double* pin_ones,
                           int32_t dtype, int32_t device, int32_t rank, int32_t world, const void* nccl_id,
                           pdd_blind** out);
+/* Multi-device blind handle (see pdd_nonblind_create_multi). */
+PDD_API int pdd_blind_create_multi(const pdd_plan* plan, const void* data, int32_t data_kind, int32_t data_on_device,
+                                   const pdd_blind_config* cfg, const double* support_mask, const double* pin_ones,
+                                   int32_t dtype, const int32_t* devices, int32_t n_devices, pdd_blind** out);
 PDD_API int pdd_blind_layout_get(const pdd_blind* h, pdd_nonblind_layout* out);
 /* init_state (blind.cpp:169-192); w0 [s][s] c128 replaces the amplitude-based initial probe, or NULL */
 PDD_API int pdd_blind_init_state(pdd_blind* h, const double* w0);
 PDD_API int pdd_blind_step(pdd_blind* h, int32_t store_z);
 /* run() from the current state; records [max_iters][3] */
 PDD_API int pdd_blind_run(pdd_blind* h, int64_t* iterations, double* records, int64_t* diverged_at);
+/* Blind run() with the per-iteration callback (see pdd_nonblind_run_cb). */
+PDD_API int pdd_blind_run_cb(pdd_blind* h, pdd_record_cb cb, void* user, int64_t* iterations, double* records,
+                             int64_t* diverged_at);
 PDD_API int pdd_blind_iterate(pdd_blind* h, int32_t n);
 /* device time of exactly n iterations (CUDA events on the solver stream) */
 PDD_API int pdd_blind_iterate_timed(pdd_blind* h, int32_t n, double* ms);
@@ -244,6 +282,12 @@ PDD_API int pdd_host_free(void* p);
  * for the allocation.  No reference counterpart (reference results are host
  * values already). */
 PDD_API int pdd_host_stage_reserve(void);
+/* Device memory is drawn from a library-private stream-ordered pool per device
+ * that keeps freed blocks mapped while any solver lives on that device (the
+ * pool is trimmed when the last one is destroyed).  This returns every unused
+ * block of every pool to the driver now (synchronises the devices used).  No
+ * reference counterpart. */
+PDD_API int pdd_release_cached_memory(void);
 
 #ifdef __cplusplus
 }

@@ -293,7 +293,7 @@ def illumination_density(probe: np.ndarray, g: ScanGeometry) -> np.ndarray:
 def probe_density(image: np.ndarray, g: ScanGeometry) -> np.ndarray:
     """forward.cpp:68-78: sum_j |image|window_j|^2, ascending j."""
     p = _patches(image, g.positions, g.frame_side)
-    out = np.zeros((g.frame_side, g.frame_side))
+    out = np.zeros((g.frame_side, g.frame_side), p.real.dtype)
     for j in range(p.shape[0]):
         out += p[j].real ** 2 + p[j].imag ** 2
     return out
@@ -303,7 +303,7 @@ def adjoint_probe(image: np.ndarray, frames: np.ndarray, g: ScanGeometry) -> np.
     """forward.cpp:80-93: sum_j conj(image|window_j) o F*(frame_j), ascending j."""
     back = ifft2n(frames)
     p = _patches(image, g.positions, g.frame_side)
-    out = np.zeros((g.frame_side, g.frame_side), complex)
+    out = np.zeros((g.frame_side, g.frame_side), back.dtype)
     for j in range(p.shape[0]):
         out += np.conj(p[j]) * back[j]
     return out
@@ -334,8 +334,9 @@ def pixel_prox(y, b, lam: float, eps: float):
     """stagm.cpp:45-73, vectorised: outer candidate clamped to eps*sqrt(b), then
     the origin, then the inner stationary point; strict < so ties keep the
     earlier candidate; phase of y with sign(0) := 1."""
-    y = np.asarray(y, complex)
-    b = np.asarray(b, float)
+    y = np.asarray(y)
+    y = y if y.dtype in (np.complex64, np.complex128) else y.astype(complex)
+    b = np.asarray(b, np.float32 if y.dtype == np.complex64 else float)
     absy = np.abs(y)
     root_b = np.sqrt(b)
     inner_edge = eps * root_b
@@ -449,6 +450,12 @@ class ConvergenceRecord:
     lagrangian: Optional[float] = None
 
 
+def _dtypes(precision: str):
+    if precision not in ("f64", "f32"):
+        raise InvalidArgument("precision must be 'f64' or 'f32'")
+    return (np.float32, np.complex64) if precision == "f32" else (np.float64, np.complex128)
+
+
 def _local_pins(plan: DecompositionPlan, pin_ones: Optional[np.ndarray]) -> List[np.ndarray]:
     """Uncovered pixels plus the caller's vacuum mask (solver.cpp:43-48,64-69)."""
     g = plan.geometry
@@ -509,15 +516,21 @@ class NonblindSolver:
     """solver.hpp:72-107 / solver.cpp."""
 
     def __init__(self, plan: DecompositionPlan, intensities: np.ndarray, probe: np.ndarray,
-                 config: NonblindConfig, pin_ones: Optional[np.ndarray] = None):
+                 config: NonblindConfig, pin_ones: Optional[np.ndarray] = None, precision: str = "f64"):
+        """precision "f32": the same restatement evaluated in numpy float32 /
+        complex64 -- not the reference (which is double throughout) but the
+        float32 floor: what float32 arithmetic itself makes of these formulas,
+        against which a float32 GPU result is judged where cancellation makes
+        the 1e-5 bound unattainable (tests/test_configs_gpu.py)."""
         config.validate()
+        self.rdt, self.cdt = _dtypes(precision)
         g = plan.geometry
         if intensities.shape != (g.frame_count(), g.frame_side, g.frame_side):
             raise InvalidArgument("FrameStack: frame count or shape mismatch")
         if (intensities < 0).any():
             raise InvalidArgument("FrameStack: negative intensity")
-        self.plan, self.probe, self.config = plan, np.asarray(probe, complex), config
-        self.frames = partition_frames(np.asarray(intensities, float), plan)
+        self.plan, self.probe, self.config = plan, np.asarray(probe, self.cdt), config
+        self.frames = partition_frames(np.asarray(intensities, self.rdt), plan)
         self.pin = _local_pins(plan, pin_ones)
         self.denom = []
         for d in range(plan.D):
@@ -535,7 +548,7 @@ class NonblindSolver:
         u, z, gamma = [], [], []
         for d in range(self.plan.D):
             lg = self.plan.local_geometries[d]
-            u.append(np.ones((lg.image_height, lg.image_width), complex))
+            u.append(np.ones((lg.image_height, lg.image_width), self.cdt))
             z.append(forward(self.probe, u[-1], lg))
             gamma.append(np.zeros_like(z[-1]))
         v, lam = [], []
@@ -675,13 +688,15 @@ class BlindSolver:
     """blind.hpp:58-85 / blind.cpp."""
 
     def __init__(self, plan: DecompositionPlan, intensities: np.ndarray, config: BlindConfig,
-                 pin_ones: Optional[np.ndarray] = None):
+                 pin_ones: Optional[np.ndarray] = None, precision: str = "f64"):
+        """precision: see NonblindSolver (w0 and the mask are always built in float64)."""
+        self.rdt, self.cdt = _dtypes(precision)
         s = plan.geometry.frame_side
         config.validate(s)
         self.plan, self.config = plan, config
         self.frames = partition_frames(np.asarray(intensities, float), plan)
         self.pin = _local_pins(plan, pin_ones)
-        self.rpen = [_overlap_penalty(plan, d, np.zeros((lg.image_height, lg.image_width)), config.r)
+        self.rpen = [_overlap_penalty(plan, d, np.zeros((lg.image_height, lg.image_width), self.rdt), config.r)
                      for d, lg in enumerate(plan.local_geometries)]
         self.sqrt_f = [np.sqrt(f) for f in self.frames]
         self.sqrt_f_l1 = float(sum(np.sum(x) for x in self.sqrt_f))
@@ -706,6 +721,8 @@ class BlindSolver:
         self.w0 = w0
         m = config.support_mask
         self.mask = m.astype(float) if (m is not None and m.size > 0) else estimate_support_mask(w0, config.support_energy)
+        self.frames = [f.astype(self.rdt) for f in self.frames]
+        self.mask = self.mask.astype(self.rdt)
 
     def project_support(self, probe: np.ndarray):
         """blind.cpp:159-167 -> (spatial, masked spectrum)."""
@@ -715,13 +732,13 @@ class BlindSolver:
 
     def init_state(self, w_init: Optional[np.ndarray] = None) -> BlindState:
         """blind.cpp:169-192 (w_init: SURVEY.md Appendix A custom initial probe)."""
-        w = self.w0.copy() if w_init is None else np.asarray(w_init, complex).copy()
+        w = (self.w0 if w_init is None else np.asarray(w_init)).astype(self.cdt)
         st = BlindState(w, [], [], [], [], [], [], [], 0)
         s = self.plan.geometry.frame_side
         for lg in self.plan.local_geometries:
             st.w_copies.append(w.copy())
-            st.delta.append(np.zeros((s, s), complex))
-            st.u.append(np.ones((lg.image_height, lg.image_width), complex))
+            st.delta.append(np.zeros((s, s), self.cdt))
+            st.u.append(np.ones((lg.image_height, lg.image_width), self.cdt))
             st.z.append(forward(w, st.u[-1], lg))
             st.gamma.append(np.zeros_like(st.z[-1]))
         for ov in self.plan.overlaps:

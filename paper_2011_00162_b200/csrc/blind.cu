@@ -83,7 +83,8 @@ class Blind final : public BlindGpu {
  public:
   Blind(const Plan& plan, const DataSpec& data, const BlindConfig& cfg, const double* mask, const double* pin_ones,
         int device, Comm* comm)
-      : plan_(plan), cfg_(cfg) {
+      : plan_(plan), cfg_(cfg), pool_(device) {
+    AllocStream alloc_scope(R.st());  // every buffer is stream-ordered on the solver stream
     cfg_.validate(plan.g.s, mask);
     plan.g.validate();
     R.build(plan, data, pin_ones, device, comm, cfg.max_iters, "BlindSolver");
@@ -344,14 +345,17 @@ class Blind final : public BlindGpu {
 
   void ensure_graphs() {
     if (full_[0].ready()) return;
+    // a host-blocking transport (test transport, Comm::capturable) runs the
+    // same bodies eagerly
+    const bool eager = R.comm && !R.comm->capturable();
     for (int p = 0; p < 2; ++p) {
-      full_[p].capture(R.st(), [&] {
+      full_[p].capture(R.st(), [this, p] {
         enqueue_iteration(p, false);
         enqueue_iteration(1 - p, false);
-      });
-      one_[p].capture(R.st(), [&] { enqueue_iteration(p, false); });
+      }, eager);
+      one_[p].capture(R.st(), [this, p] { enqueue_iteration(p, false); }, eager);
     }
-    tail_.capture(R.st(), [&] { enqueue_tail(); });
+    tail_.capture(R.st(), [this] { enqueue_tail(); }, eager);
   }
 
   void ensure_z() {
@@ -368,7 +372,9 @@ class Blind final : public BlindGpu {
     z_valid_ = store_z;
   }
 
-  std::vector<double> drive(int max_total, bool poll, bool tail = true) {
+  // on_poll(ctl, per-launch ms so far) at every poll (the stream is idle then).
+  std::vector<double> drive(int max_total, bool poll, bool tail = true,
+                            const std::function<void(const RunCtl&, const std::vector<double>&)>& on_poll = {}) {
     ensure_graphs();
     constexpr int kPoll = 8;
     cudaStream_t s = R.st();
@@ -393,7 +399,11 @@ class Blind final : public BlindGpu {
       }
       launched += 2 * batch;
       if (launched >= max_total) break;
-      if (poll && R.read_ctl().stop) break;
+      if (poll) {
+        const RunCtl c = R.read_ctl();
+        if (on_poll) on_poll(c, event_ms(ev));
+        if (c.stop) break;
+      }
     }
     PDD_CUDA(cudaStreamSynchronize(s));
     std::vector<double> ms;
@@ -411,19 +421,23 @@ class Blind final : public BlindGpu {
     return ms;
   }
 
-  RunRecords run() override {  // blind.cpp:298-358, from the current state
+  RunRecords run(const RecordFn& on_record) override {  // blind.cpp:298-358, from the current state
     refresh_wd();
     R.reset_ctl(static_cast<int>(iter_), static_cast<int>(iter_) + cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf,
                 cfg_.tol_re);
     const int64_t start = iter_;
-    const auto ms = drive(cfg_.max_iters, true);
+    RecordFeed feed{&on_record, start, start};
+    const auto ms = drive(cfg_.max_iters, true, true, [&](const RunCtl& c, const std::vector<double>& ms_now) {
+      feed.upto(R.rec.template as<double>(), R.rec_cap, R.st(), c.stop ? c.stop : c.iter - 1, ms_now);
+    });
     const RunCtl c = R.read_ctl();
     RunRecords out;
     const int64_t last = c.stop ? c.stop : c.iter;
     out.iterations = last - start;
     out.diverged_at = c.diverged ? c.diverged - start : 0;
     std::vector<double> rec(2 * static_cast<size_t>(R.rec_cap));
-    PDD_CUDA(cudaMemcpy(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+    PDD_CUDA(cudaMemcpyAsync(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost, R.st()));
+      PDD_CUDA(cudaStreamSynchronize(R.st()));
     for (int64_t n = start + 1; n <= last; ++n) {
       const int64_t k = (n - 1) % R.rec_cap;
       out.rf.push_back(rec[2 * k]);
@@ -431,6 +445,7 @@ class Blind final : public BlindGpu {
       const size_t li = static_cast<size_t>((n - start - 1) / 2);
       out.t_ms.push_back(ms.empty() ? 0.0 : ms[std::min(li, ms.size() - 1)] / 2.0);
     }
+    feed.upto(R.rec.template as<double>(), R.rec_cap, R.st(), last, ms);
     iter_ = last;
     z_valid_ = false;
     return out;
@@ -559,6 +574,7 @@ class Blind final : public BlindGpu {
   void merged(double* out) override { R.merge_to_host(plan_, u_.as<cx<T>>(), out); }
   void sync() override { R.stream.sync(); }
   // float32 s = 64: the BLIND frame pass is two streamed launches (kernels.cu)
+  void* stream() const override { return R.st(); }
   int64_t kernel_launches_per_iteration() const override {
     return std::is_same_v<T, float> && R.S == 64 ? 18 : 17;
   }
@@ -566,6 +582,7 @@ class Blind final : public BlindGpu {
  private:
   Plan plan_;
   BlindConfig cfg_;
+  PoolUser pool_;  // before every DevMem: the pool outlives them
   RankData<T> R;
   StateLayout layout_;
   DevMem gamma_[2], q_, u_, v_, lam_, s_, rpen_, z_, wc_, delta_, num_, den_, w_, avg_, spec_, wd_all_, ones_, mask_;

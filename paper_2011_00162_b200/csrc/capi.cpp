@@ -130,6 +130,11 @@ void layout_out(const pdd::StateLayout& L, pdd_nonblind_layout* out) {
   out->lambda_elems = 2 * out->v_elems;
 }
 
+pdd::RecordFn record_fn(pdd_record_cb cb, void* user) {
+  if (!cb) return {};
+  return [cb, user](int64_t it, double rf, double re, double t, double lag) { cb(it, rf, re, t, lag, user); };
+}
+
 void records_out(const pdd::RunRecords& r, int64_t* iterations, double* records, int64_t* diverged_at) {
   if (iterations) *iterations = r.iterations;
   if (diverged_at) *diverged_at = r.diverged_at;
@@ -479,7 +484,8 @@ static int nonblind_create(const pdd_plan* plan, const void* data, int32_t kind,
     DeviceScope ds(device);
     if (world > 1 || nccl_id) {  // world 1 with an id: single-rank NCCL communicator (plumbing test)
       need(nccl_id, "nccl_id");
-      h->comm = pdd::make_nccl_comm(nccl_id, rank, world, device);
+      h->comm = pdd::is_host_hub_id(nccl_id) ? pdd::make_host_comm(nccl_id, rank, world)
+                                             : pdd::make_nccl_comm(nccl_id, rank, world, device);
     }
     pdd::DataSpec spec{data, kind, on_dev != 0};
     h->s = pdd::make_nonblind(plan->plan, spec, probe, nb_cfg(cfg), pin, f64 ? 2 : 1, device, h->comm.get());
@@ -502,10 +508,40 @@ int pdd_nonblind_create_rank(const pdd_plan* plan, const void* data, int32_t dat
                          nccl_id, out);
 }
 
+int pdd_nonblind_create_multi(const pdd_plan* plan, const void* data, int32_t kind, int32_t on_dev,
+                              const double* probe, const pdd_nonblind_config* cfg, const double* pin, int32_t dtype,
+                              const int32_t* devices, int32_t n_devices, pdd_nonblind** out) {
+  return guard([&] {
+    need(plan, "plan");
+    need(data, "data");
+    need(probe, "probe");
+    need(devices, "devices");
+    need(out, "out");
+    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (n_devices < 1) throw pdd::InvalidArgument("n_devices >= 1");
+    const bool f64 = is_f64(dtype);
+    auto h = std::make_unique<pdd_nonblind>();
+    h->device = devices[0];
+    DeviceScope ds(devices[0]);
+    pdd::DataSpec spec{data, kind, on_dev != 0};
+    h->s = pdd::make_nonblind_multi(plan->plan, spec, probe, nb_cfg(cfg), pin, f64 ? 2 : 1,
+                                    std::vector<int>(devices, devices + n_devices));
+    *out = h.release();
+  });
+}
+
+int pdd_host_transport_id(void* out128) {
+  return guard([&] {
+    need(out128, "out");
+    pdd::host_hub_id(out128);
+  });
+}
+
 #define NB_CALL(h, body)                     \
   return guard([&] {                         \
     need(h, "handle");                       \
     DeviceScope ds_((h)->device);            \
+    pdd::AllocStream as_(static_cast<cudaStream_t>((h)->s->stream())); \
     body;                                    \
   })
 
@@ -544,6 +580,10 @@ int pdd_nonblind_init_state(pdd_nonblind* h) { NB_CALL(h, h->s->init_state()); }
 int pdd_nonblind_step(pdd_nonblind* h, int32_t store_z) { NB_CALL(h, h->s->step(store_z != 0)); }
 int pdd_nonblind_run(pdd_nonblind* h, int64_t* iterations, double* records, int64_t* diverged_at) {
   NB_CALL(h, records_out(h->s->run(), iterations, records, diverged_at));
+}
+int pdd_nonblind_run_cb(pdd_nonblind* h, pdd_record_cb cb, void* user, int64_t* iterations, double* records,
+                        int64_t* diverged_at) {
+  NB_CALL(h, records_out(h->s->run(record_fn(cb, user)), iterations, records, diverged_at));
 }
 int pdd_nonblind_iterate(pdd_nonblind* h, int32_t n) { NB_CALL(h, h->s->iterate(n)); }
 int pdd_nonblind_iterate_timed(pdd_nonblind* h, int32_t n, double* ms) {
@@ -619,10 +659,32 @@ static int blind_create(const pdd_plan* plan, const void* data, int32_t kind, in
     DeviceScope ds(device);
     if (world > 1 || nccl_id) {
       need(nccl_id, "nccl_id");
-      h->comm = pdd::make_nccl_comm(nccl_id, rank, world, device);
+      h->comm = pdd::is_host_hub_id(nccl_id) ? pdd::make_host_comm(nccl_id, rank, world)
+                                             : pdd::make_nccl_comm(nccl_id, rank, world, device);
     }
     pdd::DataSpec spec{data, kind, on_dev != 0};
     h->s = pdd::make_blind(plan->plan, spec, bl_cfg(cfg), mask, pin, f64 ? 2 : 1, device, h->comm.get());
+    *out = h.release();
+  });
+}
+
+int pdd_blind_create_multi(const pdd_plan* plan, const void* data, int32_t kind, int32_t on_dev,
+                           const pdd_blind_config* cfg, const double* mask, const double* pin, int32_t dtype,
+                           const int32_t* devices, int32_t n_devices, pdd_blind** out) {
+  return guard([&] {
+    need(plan, "plan");
+    need(data, "data");
+    need(devices, "devices");
+    need(out, "out");
+    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (n_devices < 1) throw pdd::InvalidArgument("n_devices >= 1");
+    const bool f64 = is_f64(dtype);
+    auto h = std::make_unique<pdd_blind>();
+    h->device = devices[0];
+    DeviceScope ds(devices[0]);
+    pdd::DataSpec spec{data, kind, on_dev != 0};
+    h->s = pdd::make_blind_multi(plan->plan, spec, bl_cfg(cfg), mask, pin, f64 ? 2 : 1,
+                                 std::vector<int>(devices, devices + n_devices));
     *out = h.release();
   });
 }
@@ -651,6 +713,10 @@ int pdd_blind_init_state(pdd_blind* h, const double* w0) { NB_CALL(h, h->s->init
 int pdd_blind_step(pdd_blind* h, int32_t store_z) { NB_CALL(h, h->s->step(store_z != 0)); }
 int pdd_blind_run(pdd_blind* h, int64_t* iterations, double* records, int64_t* diverged_at) {
   NB_CALL(h, records_out(h->s->run(), iterations, records, diverged_at));
+}
+int pdd_blind_run_cb(pdd_blind* h, pdd_record_cb cb, void* user, int64_t* iterations, double* records,
+                     int64_t* diverged_at) {
+  NB_CALL(h, records_out(h->s->run(record_fn(cb, user)), iterations, records, diverged_at));
 }
 int pdd_blind_iterate(pdd_blind* h, int32_t n) { NB_CALL(h, h->s->iterate(n)); }
 int pdd_blind_iterate_timed(pdd_blind* h, int32_t n, double* ms) {
@@ -694,6 +760,9 @@ int pdd_host_alloc(void** p, int64_t bytes) {
     need(p, "p");
     pdd::cuda_check(cudaMallocHost(p, static_cast<size_t>(bytes)), "cudaMallocHost");
   });
+}
+int pdd_release_cached_memory(void) {
+  return guard([&] { pdd::release_cached_memory(); });
 }
 int pdd_host_stage_reserve(void) {
   return guard([&] { pdd::host_stage_reserve(); });

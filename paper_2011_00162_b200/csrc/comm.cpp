@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "device.hpp"
@@ -32,17 +33,31 @@ struct NcclApi {
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
 
+  // Resolved once per process (thread-safe); a failed resolution leaves no
+  // half-initialised table behind and is reported again on every use.
   static NcclApi& get() {
     static NcclApi api;
-    if (!api.h) api.load();
+    static std::string failure;
+    static std::once_flag once;
+    std::call_once(once, [] {
+      try {
+        api.load();
+      } catch (const std::exception& e) {
+        failure = e.what();
+      }
+    });
+    if (!failure.empty()) throw RuntimeError(failure);
     return api;
   }
   void load() {
-    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) throw RuntimeError(std::string("NCCL unavailable: ") + dlerror());
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) throw RuntimeError(std::string("NCCL unavailable: ") + dlerror());
     auto sym = [&](const char* n) {
-      void* p = dlsym(h, n);
-      if (!p) throw RuntimeError(std::string("NCCL symbol missing: ") + n);
+      void* p = dlsym(lib, n);
+      if (!p) {
+        dlclose(lib);
+        throw RuntimeError(std::string("NCCL symbol missing: ") + n);
+      }
       return p;
     };
     get_unique_id = reinterpret_cast<decltype(get_unique_id)>(sym("ncclGetUniqueId"));
@@ -54,6 +69,7 @@ struct NcclApi {
     recv = reinterpret_cast<decltype(recv)>(sym("ncclRecv"));
     allreduce = reinterpret_cast<decltype(allreduce)>(sym("ncclAllReduce"));
     error_string = reinterpret_cast<decltype(error_string)>(sym("ncclGetErrorString"));
+    h = lib;  // published only once every symbol resolved
   }
   void check(ncclResult_t r, const char* what) const {
     if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + error_string(r));

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -196,6 +197,105 @@ void upload_cx(void* dev, const double* src, int64_t n, cudaStream_t st) {
 }
 
 
+// Page-locks a caller's pageable host buffer for the duration of one upload
+// (DMA at full PCIe/C2C rate instead of staged pageable copies).  Process-wide
+// registry: concurrent uploads from the same buffer share one registration,
+// which is dropped by the last of them only after its stream has drained;
+// buffers page-locked by someone else are used as they are.  The destructor
+// covers the exception paths.
+class HostPin {
+ public:
+  HostPin(const void* p, size_t bytes, cudaStream_t st) : p_(p), st_(st) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(mu());
+    auto& reg = table();
+    if (auto it = reg.find(p); it != reg.end()) {
+      if (it->second.bytes >= bytes) {
+        ++it->second.users;
+        mine_ = true;
+      }
+      return;
+    }
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeUnregistered &&
+        cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterReadOnly) == cudaSuccess) {
+      reg[p] = Entry{bytes, 1};
+      mine_ = true;
+    }
+    cudaGetLastError();
+  }
+  ~HostPin() { done(); }
+  HostPin(const HostPin&) = delete;
+  HostPin& operator=(const HostPin&) = delete;
+  // Drain this upload's stream, then drop this user's share of the registration.
+  void done() noexcept {
+    if (!mine_) return;
+    mine_ = false;
+    cudaStreamSynchronize(st_);
+    std::lock_guard<std::mutex> lock(mu());
+    auto& reg = table();
+    auto it = reg.find(p_);
+    if (it != reg.end() && --it->second.users == 0) {
+      cudaHostUnregister(const_cast<void*>(p_));
+      reg.erase(it);
+    }
+    cudaGetLastError();
+  }
+
+ private:
+  struct Entry {
+    size_t bytes;
+    int users;
+  };
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::map<const void*, Entry>& table() {
+    static std::map<const void*, Entry> t;
+    return t;
+  }
+  const void* p_;
+  cudaStream_t st_;
+  bool mine_ = false;
+};
+
+// Streams run() records to a RecordFn as the device completes them.
+struct RecordFeed {
+  const RecordFn* cb = nullptr;
+  int64_t start = 0;      // iteration count before this run
+  int64_t delivered = 0;  // absolute iteration of the last record handed out
+  // Hand out records start+1.. last (absolute).  rec: the device record ring
+  // [rec_cap][2] (rf, re); ms: device ms per 2-iteration launch so far.
+  void upto(const double* dev_rec, int rec_cap, cudaStream_t st, int64_t last, const std::vector<double>& ms,
+            const std::vector<double>* lag = nullptr) {
+    if (!cb || !*cb) return;
+    if (delivered < start) delivered = start;
+    if (last <= delivered) return;
+    std::vector<double> rec(2 * static_cast<size_t>(rec_cap));
+    PDD_CUDA(cudaMemcpyAsync(rec.data(), dev_rec, sizeof(double) * rec.size(), cudaMemcpyDeviceToHost, st));
+    PDD_CUDA(cudaStreamSynchronize(st));
+    for (int64_t n = delivered + 1; n <= last; ++n) {
+      const int64_t k = (n - 1) % rec_cap, i = n - start;
+      const double t = ms.empty() ? 0.0 : ms[std::min<size_t>(static_cast<size_t>((i - 1) / 2), ms.size() - 1)] / 2.0;
+      const double L = lag && i - 1 < static_cast<int64_t>(lag->size()) ? (*lag)[i - 1] : NAN;
+      (*cb)(i, rec[2 * k], rec[2 * k + 1], t, L);
+    }
+    delivered = last;
+  }
+};
+
+// Device ms between consecutive events (all recorded work complete).
+inline std::vector<double> event_ms(const std::vector<cudaEvent_t>& ev) {
+  std::vector<double> ms;
+  for (size_t i = 1; i < ev.size(); ++i) {
+    float t = 0.f;
+    PDD_CUDA(cudaEventElapsedTime(&t, ev[i - 1], ev[i]));
+    ms.push_back(t);
+  }
+  return ms;
+}
+
 template <typename T>
 struct RankData {
   Layout L;
@@ -208,6 +308,7 @@ struct RankData {
   DevMem sub_fr_beg, sub_tile_beg, local_map;
   DevMem pc_beg, pc_pos, pc_ofs, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
+  DevMem scratch;  // global transpose tiles of the streamed kernel (complex128 128^2 frames)
   DevMem ctl, rec;
   DevMem pin_dev;  // uint8 per local image pixel
   double l1 = 0.0;
@@ -239,7 +340,7 @@ struct RankData {
     if (!frame_supported<T>(S))
       throw InvalidArgument(std::string(who) + ": frame side " + std::to_string(S) +
                             " not supported by the CUDA path (powers of two up to " +
-                            (sizeof(T) == 4 ? "128" : "64") + ")");
+                            "128)");
     cudaStream_t s = st();
     tw = upload(twiddles<T>(S), s);
     fr_off = upload(L.fr_off, s);
@@ -262,6 +363,7 @@ struct RankData {
     sub_fr_beg = upload(L.sub_fr_beg, s);
     sub_tile_beg = upload(L.sub_tile_beg, s);
     local_map = upload(L.local_subs, s);
+    if (const size_t b = stream_scratch_bytes<T>(S)) scratch.alloc(b, s);
     if (const int G = sweep_stream_ctas<T>(S); G > 0) {  // the streamed sweep's schedule
       L.schedule(G);
       pc_beg = upload(L.cta_beg, s);
@@ -305,15 +407,8 @@ struct RankData {
     const char* src = static_cast<const char*>(data.ptr);
     // Pageable host input: page-lock it for the duration of the upload (DMA at
     // full PCIe/C2C rate instead of staged pageable copies).
-    bool registered = false;
     const size_t total = static_cast<size_t>(plan.g.J()) * per * esz;
-    if (!data.device && total >= (size_t(64) << 20)) {
-      cudaPointerAttributes at{};
-      if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeUnregistered) {
-        registered = cudaHostRegister(const_cast<char*>(src), total, cudaHostRegisterReadOnly) == cudaSuccess;
-      }
-      cudaGetLastError();
-    }
+    HostPin pin_src(data.device || total < (size_t(64) << 20) ? nullptr : src, total, s);
     auto runs = [&](int64_t f0, int64_t f1, char* dst) {  // runs of consecutive global frames
       int64_t f = f0;
       while (f < f1) {
@@ -340,9 +435,10 @@ struct RankData {
         PDD_CUDA(cudaStreamSynchronize(s));  // stage reuse
       }
     }
-    if (registered) cudaHostUnregister(const_cast<char*>(src));
+    pin_src.done();
     unsigned long long nneg = 0;
-    PDD_CUDA(cudaMemcpy(&nneg, neg.get(), sizeof(nneg), cudaMemcpyDeviceToHost));
+    PDD_CUDA(cudaMemcpyAsync(&nneg, neg.get(), sizeof(nneg), cudaMemcpyDeviceToHost, s));
+    PDD_CUDA(cudaStreamSynchronize(s));
     if (nneg) throw InvalidArgument("FrameStack: negative intensity");
     // l1 = sum_d sum_j sum_i sqrt(f)
     DevMem fs(sizeof(double) * std::max<int64_t>(L.nfr, 1));
@@ -400,6 +496,7 @@ struct RankData {
     a.scale = static_cast<T>(1.0 / static_cast<double>(S));
     a.rows_al16 = rows_al16 ? 1 : 0;
     a.img_elems = L.img_elems;
+    a.scratch = scratch.as<cx<T>>();
     return a;
   }
 

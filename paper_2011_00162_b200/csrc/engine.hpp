@@ -38,6 +38,13 @@ struct DataSpec {
   bool device = false;
 };
 
+// Per-iteration record delivered while run() executes (solver.hpp:88
+// on_iteration): 1-based iteration, R-factor, relative error, iteration time
+// (device ms), augmented Lagrangian (NaN unless record_lagrangian).  Records
+// arrive in order, each once, at most a poll window (16 iterations) after the
+// device produced them, and never for iterations a stop rule rolls back.
+using RecordFn = std::function<void(int64_t iteration, double rf, double re, double t_ms, double lag)>;
+
 struct RunRecords {
   int64_t iterations = 0;
   int64_t diverged_at = 0;  // > 0: non-finite RF/RE at this iteration
@@ -58,10 +65,20 @@ struct Comm {
   virtual void recv(void* buf, size_t bytes, int peer, void* stream) = 0;
   virtual void allreduce_sum_f64(double* buf, size_t n, void* stream) = 0;
   virtual void allreduce_sum_f32(float* buf, size_t n, void* stream) = 0;
+  // false: calls block on the host (they synchronise the stream and wait for
+  // peers), so the iteration runs eagerly instead of as a CUDA graph
+  virtual bool capturable() const { return true; }
 };
 
 std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int world, int device);
 void nccl_unique_id(void* out128);
+// In-process host-staged transport between ranks that are threads of one
+// process (any devices, including one device shared by every rank): the
+// multi-rank path of the solvers without NCCL, for testing it on one GPU.
+// Ranks passing the same hub id form one world.
+std::unique_ptr<Comm> make_host_comm(const void* hub_id128, int rank, int world);
+void host_hub_id(void* out128);
+bool is_host_hub_id(const void* id128);
 
 struct StateLayout {
   std::vector<int> local_subs;        // global subdomain ids owned here
@@ -80,7 +97,7 @@ class NonblindGpu {
   // One iteration (solver.cpp:118-205).  store_z keeps z for get_state.
   virtual void step(bool store_z) = 0;
   // Config-driven solve from the current state (solver.cpp:216-267), stop rules on device.
-  virtual RunRecords run() = 0;
+  virtual RunRecords run(const RecordFn& on_record = {}) = 0;
   // Exactly n iterations from the current state, no stop rule (benchmark path).
   virtual void iterate(int n) = 0;
   // Same, returning the device time (CUDA events on the solver stream) in ms.
@@ -101,6 +118,7 @@ class NonblindGpu {
   virtual std::vector<double> lagrangian_history() const = 0;
   virtual void merged(double* out) = 0;         // merge() of the current sub-solutions (single rank)
   virtual void sync() = 0;
+  virtual void* stream() const = 0;  // cudaStream_t of this rank's work
   virtual int64_t kernel_launches_per_iteration() const = 0;
 };
 
@@ -119,7 +137,7 @@ class BlindGpu {
   virtual const StateLayout& layout() const = 0;
   virtual void init_state(const double* w0) = 0;  // nullptr: the solver's amplitude-based w0
   virtual void step(bool store_z) = 0;
-  virtual RunRecords run() = 0;
+  virtual RunRecords run(const RecordFn& on_record = {}) = 0;
   virtual void iterate(int n) = 0;
   virtual double iterate_timed(int n) = 0;          // device ms of exactly n iterations
   virtual void profile(int n, double* ms) = 0;      // {frame kernel, u-gather, iteration} averages
@@ -131,10 +149,21 @@ class BlindGpu {
   virtual void get_probe(double* probe, double* probe_fourier, double* mask, double* w0) = 0;
   virtual void merged(double* out) = 0;
   virtual void sync() = 0;
+  virtual void* stream() const = 0;  // cudaStream_t of this rank's work
   virtual int64_t kernel_launches_per_iteration() const = 0;
 };
 
 std::unique_ptr<BlindGpu> make_blind(const Plan& plan, const DataSpec& data, const BlindConfig& cfg,
                                      const double* mask, const double* pin_ones, int dtype, int device, Comm* comm);
+
+// One handle over G = devices.size() ranks of this process (multi.cpp): rank
+// r on devices[r], NCCL between distinct devices, the host transport when a
+// device repeats.  State in the single-handle layout.
+std::unique_ptr<NonblindGpu> make_nonblind_multi(const Plan& plan, const DataSpec& data, const double* probe,
+                                                 const NonblindConfig& cfg, const double* pin_ones, int dtype,
+                                                 const std::vector<int>& devices);
+std::unique_ptr<BlindGpu> make_blind_multi(const Plan& plan, const DataSpec& data, const BlindConfig& cfg,
+                                           const double* mask, const double* pin_ones, int dtype,
+                                           const std::vector<int>& devices);
 
 }  // namespace pdd

@@ -58,6 +58,8 @@ struct FrameArgs {
   const int4* pc_pos = nullptr;       // [nframes] {frame, lo, newfrom, rot}
   const int64_t* pc_ofs = nullptr;    // [nframes]
   int64_t img_elems = 0;              // PDD_BOUNDS builds: image buffer size (elements)
+  cx<T>* scratch = nullptr;           // global transpose tiles of the streamed kernel when its
+                                      // tile exceeds shared memory (stream_scratch_bytes)
 };
 
 // ST-AGM per-pixel prox, stagm.cpp:45-73.  amp = sqrt(b).  The fast form is

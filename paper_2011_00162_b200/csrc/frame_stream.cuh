@@ -99,9 +99,19 @@ constexpr bool amp_tile_staged() {
 template <typename T, class SH>
 constexpr size_t stream_smem_bytes_base();
 
+// Shapes whose transpose tile does not fit in shared memory (complex128
+// 128^2: 272 KB) keep it in a per-CTA global scratch slice instead
+// (a.scratch + blockIdx.x * S * P; L2-resident: ~80 MB for the whole grid).
+template <typename T, class SH>
+constexpr bool tile_in_global() {
+  return sizeof(cx<T>) * static_cast<size_t>(SH::S) * SH::P > (size_t(160) << 10);
+}
+
 // FWD = true: the forward half only (FrameMode kFwd: A u -> frames_out,
 // |A u|^2 -> inten_out, R-factor partials), e.g. the trailing R-factor pass.
-template <typename T, class SH, bool FAST, bool TMEMP = false, bool FWD = false>
+// ADJ = true: the inverse half only (FrameMode kAdj: frames_in -> IFFT2 ->
+// x conj(probe) -> bp_out per frame), global-tile shapes only.
+template <typename T, class SH, bool FAST, bool TMEMP = false, bool FWD = false, bool ADJ = false>
 __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const FrameArgs<T> a) {
   constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
@@ -114,8 +124,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
   cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
   cx<T>* twc = twr + S;  // column-phase twiddles, [gc][k] = W_S^(gc k): immediate offsets in k
-  cx<T>* buf = twc + S;
-  double* red = reinterpret_cast<double*>(buf + S * P);
+  constexpr bool GTILE = tile_in_global<T, SH>();
+  static_assert(!ADJ || GTILE, "ADJ: global-tile shapes only");
+  static_assert(!(GTILE && TMEMP), "global tile: no tensor-memory paths");
+  cx<T>* buf = GTILE ? a.scratch + static_cast<int64_t>(blockIdx.x) * S * P : twc + S;
+  double* red = reinterpret_cast<double*>(GTILE ? twc + S : buf + S * P);
   // S = 128: the amplitudes of the next column group land by cp.async straight
   // in shared memory ([element][thread], conflict-free, read back only by the
   // thread that copied them) -- the column phase sits at the 128-register cap
@@ -189,7 +202,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // pitches; checked on the host).
   constexpr int NW = NT / 32;
   __shared__ __align__(8) uint64_t s_rowbar[NW * NRB];
-  const bool tma_rows = !FWD && a.rows_al16 != 0 && sizeof(cx<T>) * S % 16 == 0;
+  const bool tma_rows = !FWD && !ADJ && !GTILE && a.rows_al16 != 0 && sizeof(cx<T>) * S % 16 == 0;
   if (tma_rows) {
     if (t < NW * NRB) mbar_init(s_rowbar + t, 1);
     mbar_init_fence();
@@ -247,7 +260,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #endif
     // one base pointer per array; the (ky - gc) * S offsets are immediates
     const int64_t base = static_cast<int64_t>(ff) * S * S + gc * S + grp * CG + cx_;
-    const cx<T>* gsrc = a.gamma_in + base;
+    const cx<T>* gsrc = (ADJ ? a.frames_in : a.gamma_in) + base;
     const T* asrc = a.amp + base;
 #pragma unroll
     for (int q = 0; q < RC / GC; ++q)
@@ -255,6 +268,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k1 = 0; k1 < GC; ++k1) {
         const int oy = GC * q + RC * k1;
         if constexpr (!FWD) pg[q * GC + k1] = gsrc[oy * S];
+        if constexpr (ADJ) continue;
         if (!FWD || a.rf_part) {
           if constexpr (STAGE) cp_async4(ampst + (q * GC + k1) * NT + t, asrc + oy * S);
           else pa[q * GC + k1] = asrc[oy * S];
@@ -270,14 +284,15 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // Work order.  SWEEP: this CTA's positions [cta_beg[b], cta_beg[b+1]) of the
   // host schedule (frames in back-projection piece order; layout.hpp).
   // FWD: frames blockIdx.x + k * gridDim.x.
-  int i = FWD ? static_cast<int>(blockIdx.x) : a.cta_beg[blockIdx.x];
-  const int iend = FWD ? a.nframes : a.cta_beg[blockIdx.x + 1];
+  constexpr bool STRIDED = FWD || ADJ;  // frames blockIdx.x + k * gridDim.x (no piece schedule)
+  int i = STRIDED ? static_cast<int>(blockIdx.x) : a.cta_beg[blockIdx.x];
+  const int iend = STRIDED ? a.nframes : a.cta_beg[blockIdx.x + 1];
   constexpr int kStepOne = 1;
   auto frame_at = [&](int j) {
-    if constexpr (FWD) return j < iend ? j : -1;
+    if constexpr (STRIDED) return j < iend ? j : -1;
     else return j < iend ? a.pc_pos[j].x : -1;
   };
-  auto next_of = [&](int j) { return FWD ? j + static_cast<int>(gridDim.x) : j + kStepOne; };
+  auto next_of = [&](int j) { return STRIDED ? j + static_cast<int>(gridDim.x) : j + kStepOne; };
   {
     const int f0 = frame_at(i);
     prefetch(f0, 0);
@@ -345,7 +360,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
     }
   };
-  constexpr bool FUSE = PDD_ROWFUSE && !FWD;
+  constexpr bool FUSE = PDD_ROWFUSE && !FWD && !ADJ;
   int pend_f = -1;  // FUSE: frame whose R-factor warp partials sit in red[]
   if constexpr (FUSE) {
     if (i < iend) fwd_rows(frame_at(i));
@@ -359,7 +374,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       __trap();
     }
 #endif
-    if constexpr (!FUSE) fwd_rows(f);
+    if constexpr (!FUSE && !ADJ) fwd_rows(f);
     if constexpr (ACC) tmem_fence_before_sync();
     __syncthreads();
     if constexpr (ACC) tmem_fence_after_sync();
@@ -378,6 +393,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int grp = 0; grp < NG; ++grp) {
       const int x = grp * CG + cx_;
       cx<T> w[RC];
+      if constexpr (ADJ) {
+        // frames_in of this column group, in the layout the forward column
+        // transform ends in: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
+#pragma unroll
+        for (int e = 0; e < RC; ++e) w[e] = pg[e];
+        if (grp + 1 < NG) prefetch(f, grp + 1);
+        else prefetch(frame_at(next_of(i)), 0);
+      } else {
 #pragma unroll
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
       dft<RC, false>(w);
@@ -445,6 +468,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       rf_acc += acc;
       if (grp + 1 < NG) prefetch(f, grp + 1);
       else prefetch(frame_at(next_of(i)), 0);
+      }  // !ADJ
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
         const int k2 = gc + GC * q;
@@ -473,7 +497,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     // this frame's piece bookkeeping: rows y < lo are final, rows y >= newfrom new
     int p_lo = S, p_new = 0, p_rot = 0;
     int64_t p_ofs = fbase;
-    if constexpr (!FWD) {
+    if constexpr (!STRIDED) {
       const int4 pi = a.pc_pos[i];
       p_lo = pi.y;
       p_new = pi.z;
@@ -616,13 +640,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 
 template <typename T, class SH>
 constexpr size_t stream_smem_bytes_base() {
-  return sizeof(cx<T>) * (3 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32) +
+  return sizeof(cx<T>) * (3 * SH::S + (tile_in_global<T, SH>() ? 0 : static_cast<size_t>(SH::S) * SH::P)) +
+         sizeof(double) * (SH::NT / 32) +
          (amp_tile_staged<T, SH, false>() ? sizeof(T) * static_cast<size_t>(SH::RC) * SH::NT : 0);
 }
 template <typename T, class SH>
 size_t stream_smem_bytes() {
-  return sizeof(cx<T>) * (3 * SH::S + static_cast<size_t>(SH::S) * SH::P) + sizeof(double) * (SH::NT / 32) +
-         (amp_tile_staged<T, SH, false>() ? sizeof(T) * static_cast<size_t>(SH::RC) * SH::NT : 0)
+  return stream_smem_bytes_base<T, SH>()
 #ifdef PDD_CANARY
          + (size_t(48) << 10)  // debug builds: a canary region after the working set
 #endif

@@ -50,11 +50,18 @@ struct StreamPick {
 };
 template <> struct StreamPick<float, 128> { using type = StreamShape<128, 512, 8, 8>; };
 template <> struct StreamPick<float, 64> { using type = StreamShape<64, 256, 4, 8, 2>; };
+// complex128 128^2: 16 values per thread on both axes (64 registers), the
+// transpose tile in global scratch (tile_in_global), 8 warps per CTA.
+template <> struct StreamPick<double, 128> { using type = StreamShape<128, 256, 8, 8, 1>; };
 
-template <typename T, class SH, bool FAST, bool FWD = false>
+template <typename T, class SH>
+constexpr bool stream_tmem_probe() {  // TMEM probe cache where it keeps occupancy (one CTA per SM)
+  return std::is_same_v<T, float> && SH::MINB == 1;
+}
+
+template <typename T, class SH, bool FAST, bool FWD = false, bool ADJ = false>
 static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
-  // TMEM probe cache where it keeps occupancy (one persistent CTA per SM)
-  auto kern = sweep_stream_kernel<T, SH, FAST, std::is_same_v<T, float> && SH::MINB == 1, FWD>;
+  auto kern = sweep_stream_kernel<T, SH, FAST, stream_tmem_probe<T, SH>(), FWD, ADJ>;
   const size_t smem = stream_smem_bytes<T, SH>();
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -70,8 +77,10 @@ static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
   }
   if (a.nframes <= 0) return cudaSuccess;
   // SWEEP runs the host schedule, built for exactly this grid
-  if (!FWD && (!a.cta_beg || a.ncta != blocks_per_sm * sms)) return cudaErrorInvalidConfiguration;
-  const int grid = FWD ? std::min(a.nframes, blocks_per_sm * sms) : a.ncta;
+  if (!FWD && !ADJ && (!a.cta_beg || a.ncta != blocks_per_sm * sms)) return cudaErrorInvalidConfiguration;
+  // global transpose tiles: one per CTA of the full persistent grid
+  if (tile_in_global<T, SH>() && !a.scratch) return cudaErrorInvalidValue;
+  const int grid = (FWD || ADJ) ? std::min(a.nframes, blocks_per_sm * sms) : a.ncta;
   kern<<<grid, SH::NT, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -98,11 +107,31 @@ int sweep_stream_ctas(int S) {
       using SH = StreamPick<float, 64>::type;
       return q(sweep_stream_kernel<float, SH, true, SH::MINB == 1, false>, SH::NT, stream_smem_bytes<float, SH>());
     }
+  } else {
+    if (S == 128) {
+      using SH = StreamPick<double, 128>::type;
+      return q(sweep_stream_kernel<double, SH, true, false, false>, SH::NT, stream_smem_bytes<double, SH>());
+    }
   }
   return 0;
 }
 template int sweep_stream_ctas<float>(int);
 template int sweep_stream_ctas<double>(int);
+
+// Bytes of global transpose-tile scratch the streamed kernels of side S need
+// (0: their tile lives in shared memory): one tile per CTA of the persistent grid.
+template <typename T>
+size_t stream_scratch_bytes(int S) {
+  if constexpr (std::is_same_v<T, double>) {
+    if (S == 128) {
+      using SH = StreamPick<double, 128>::type;
+      return sizeof(cx<double>) * static_cast<size_t>(SH::S) * SH::P * static_cast<size_t>(sweep_stream_ctas<T>(S));
+    }
+  }
+  return 0;
+}
+template size_t stream_scratch_bytes<float>(int);
+template size_t stream_scratch_bytes<double>(int);
 
 template <typename T, int S, int MODE>
 static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
@@ -114,9 +143,13 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
     using SH = typename StreamPick<T, S>::type;
     return a.fast_prox ? launch_stream<T, SH, true, true>(a, st) : launch_stream<T, SH, false, true>(a, st);
   }
+  if constexpr (MODE == kAdj && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
+    using SH = typename StreamPick<T, S>::type;
+    if constexpr (tile_in_global<T, SH>()) return launch_stream<T, SH, true, false, true>(a, st);
+  }
   if constexpr (MODE == kBlind && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
     using SH = typename StreamPick<T, S>::type;
-    if constexpr (SH::MINB > 1) {  // no TMEM probe cache: per-frame probe tiles are fine
+    if constexpr (!stream_tmem_probe<T, SH>()) {  // no TMEM probe cache: per-frame probe tiles are fine
       // BLIND = R-factor forward with the shared probe w (probe2), then the
       // SWEEP with the subdomain copies W_d and raw q_j output
       FrameArgs<T> rf = a;
@@ -132,6 +165,9 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
       return a.fast_prox ? launch_stream<T, SH, true>(sw, st) : launch_stream<T, SH, false>(sw, st);
     }
   }
+  if constexpr (std::is_same_v<T, double> && S == 128) {
+    return cudaErrorInvalidValue;  // every mode runs the streamed kernel above
+  } else {
   using C = FrameCfg<T, S>;
   using E = Fft2<T, S, C::R>;
   constexpr int threads = E::NT * C::FPB;
@@ -148,6 +184,7 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
   const int grid = (a.nframes + C::FPB - 1) / C::FPB;
   kern<<<grid, threads, smem, st>>>(a);
   return cudaGetLastError();
+  }
 }
 
 template <typename T, int S>
@@ -167,7 +204,7 @@ bool frame_supported<float>(int S) {
 }
 template <>
 bool frame_supported<double>(int S) {
-  return S == 2 || S == 4 || S == 8 || S == 16 || S == 32 || S == 64;
+  return S == 2 || S == 4 || S == 8 || S == 16 || S == 32 || S == 64 || S == 128;
 }
 
 template <>
@@ -192,6 +229,7 @@ cudaError_t launch_frame<double>(int mode, int S, const FrameArgs<double>& a, cu
     case 16: return launch_frame_mode<double, 16>(mode, a, st);
     case 32: return launch_frame_mode<double, 32>(mode, a, st);
     case 64: return launch_frame_mode<double, 64>(mode, a, st);
+    case 128: return launch_frame_mode<double, 128>(mode, a, st);
   }
   return cudaErrorInvalidValue;
 }

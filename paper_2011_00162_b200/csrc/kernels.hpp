@@ -84,6 +84,8 @@ cudaError_t launch_frame(int mode, int S, const FrameArgs<T>& a, cudaStream_t st
 template <typename T>
 int sweep_stream_ctas(int S);  // persistent grid of the streamed SWEEP kernel (0: not streamed)
 template <typename T>
+size_t stream_scratch_bytes(int S);  // global transpose tiles the streamed kernels need (0: none)
+template <typename T>
 bool frame_supported(int S);
 
 template <typename T>

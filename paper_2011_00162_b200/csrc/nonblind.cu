@@ -39,7 +39,8 @@ class Nonblind final : public NonblindGpu {
  public:
   Nonblind(const Plan& plan, const DataSpec& data, const double* probe, const NonblindConfig& cfg,
            const double* pin_ones, int device, Comm* comm)
-      : plan_(plan), cfg_(cfg) {
+      : plan_(plan), cfg_(cfg), pool_(device) {
+    AllocStream alloc_scope(R.st());  // every buffer is stream-ordered on the solver stream
     cfg_.validate();
     plan.g.validate();
     R.build(plan, data, pin_ones, device, comm, cfg.max_iters, "NonblindSolver", piece_length(plan, device));
@@ -220,13 +221,16 @@ class Nonblind final : public NonblindGpu {
 
   void ensure_graphs() {
     if (full_[0].ready()) return;
+    // a host-blocking transport (test transport, Comm::capturable) runs the
+    // same bodies eagerly
+    const bool eager = R.comm && !R.comm->capturable();
     for (int p = 0; p < 2; ++p) {
-      full_[p].capture(R.st(), [&] {
+      full_[p].capture(R.st(), [this, p] {
         enqueue_iteration(p, false);
         enqueue_iteration(1 - p, false);
-      });
-      tail_[p].capture(R.st(), [&] { enqueue_tail(p); });
-      one_[p].capture(R.st(), [&] { enqueue_iteration(p, false); });
+      }, eager);
+      tail_[p].capture(R.st(), [this, p] { enqueue_tail(p); }, eager);
+      one_[p].capture(R.st(), [this, p] { enqueue_iteration(p, false); }, eager);
     }
   }
 
@@ -245,7 +249,9 @@ class Nonblind final : public NonblindGpu {
 
   // Launch iteration-pair graphs until the device reports a stop; poll every
   // kPoll launches.  Returns per-launch milliseconds.
-  std::vector<double> drive(int max_total, bool poll, bool tail = true) {
+  // on_poll(ctl, per-launch ms so far) at every poll (the stream is idle then).
+  std::vector<double> drive(int max_total, bool poll, bool tail = true,
+                            const std::function<void(const RunCtl&, const std::vector<double>&)>& on_poll = {}) {
     ensure_graphs();
     constexpr int kPoll = 8;
     cudaStream_t s = R.st();
@@ -275,7 +281,11 @@ class Nonblind final : public NonblindGpu {
       }
       launched += 2 * batch;
       if (launched >= max_total) break;
-      if (poll && R.read_ctl().stop) break;
+      if (poll) {
+        const RunCtl c = R.read_ctl();
+        if (on_poll) on_poll(c, event_ms(ev));
+        if (c.stop) break;
+      }
     }
     PDD_CUDA(cudaStreamSynchronize(s));
     for (size_t i = 1; i < ev.size(); ++i) {
@@ -339,8 +349,20 @@ class Nonblind final : public NonblindGpu {
 
   // run() with record_lagrangian: eager iterations, z kept, L recorded after
   // each completed iteration (the reference's run loop, solver.cpp:258-260).
-  RunRecords run_recording() {
+  RunRecords run_recording(const RecordFn& cb) {
     using clk = std::chrono::steady_clock;
+    // records of iteration k complete after iteration k+1 (lagged R-factor)
+    auto deliver = [&](int64_t upto, const std::vector<double>& lag, const std::vector<double>& tms) {
+      if (!cb || upto < 1) return;
+      std::vector<double> rec(2 * static_cast<size_t>(upto));
+      PDD_CUDA(cudaMemcpyAsync(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost, R.st()));
+      PDD_CUDA(cudaStreamSynchronize(R.st()));
+      for (int64_t n = delivered_ + 1; n <= upto; ++n)
+        cb(n, rec[2 * (n - 1)], rec[2 * (n - 1) + 1], n - 1 < static_cast<int64_t>(tms.size()) ? tms[n - 1] : 0.0,
+           n - 1 < static_cast<int64_t>(lag.size()) ? lag[n - 1] : NAN);
+      delivered_ = std::max(delivered_, upto);
+    };
+    delivered_ = 0;
     ensure_z();
     init_state();
     R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
@@ -356,6 +378,7 @@ class Nonblind final : public NonblindGpu {
       tms.push_back(std::chrono::duration<double, std::milli>(clk::now() - t0).count());
       lag.push_back(lagrangian());
       if (c.stop) break;
+      deliver(c.iter - 1, lag, tms);
     }
     enqueue_tail(static_cast<int>(iter_ & 1));
     PDD_CUDA(cudaStreamSynchronize(R.st()));
@@ -365,25 +388,31 @@ class Nonblind final : public NonblindGpu {
     out.diverged_at = c.diverged;
     std::vector<double> rec(2 * static_cast<size_t>(out.iterations));
     if (out.iterations)
-      PDD_CUDA(cudaMemcpy(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+      PDD_CUDA(cudaMemcpyAsync(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost, R.st()));
+      PDD_CUDA(cudaStreamSynchronize(R.st()));
     for (int64_t n = 0; n < out.iterations; ++n) {
       out.rf.push_back(rec[2 * n]);
       out.re.push_back(rec[2 * n + 1]);
       out.t_ms.push_back(n < static_cast<int64_t>(tms.size()) ? tms[n] : 0.0);
       out.lag.push_back(n < static_cast<int64_t>(lag.size()) ? lag[n] : NAN);
     }
+    deliver(out.iterations, lag, tms);
     iter_ = out.iterations;
     last_lag_ = out.lag;
     return out;
   }
 
-  RunRecords run() override {  // solver.cpp:216-267
-    if (cfg_.record_lagrangian) return run_recording();
+  RunRecords run(const RecordFn& on_record) override {  // solver.cpp:216-267
+    if (cfg_.record_lagrangian) return run_recording(on_record);
     SetupTimer tm;
     init_state();
     R.reset_ctl(0, cfg_.max_iters, cfg_.stop_rule, cfg_.tol_rf, cfg_.tol_re);
     tm.mark("run: init");
-    const auto ms = drive(cfg_.max_iters, true);
+    RecordFeed feed{&on_record, 0, 0};
+    const auto ms = drive(cfg_.max_iters, true, true, [&](const RunCtl& c, const std::vector<double>& ms_now) {
+      // rf of iterate n is recorded by iteration n + 1's frame pass
+      feed.upto(R.rec.template as<double>(), R.rec_cap, R.st(), c.stop ? c.stop : c.iter - 1, ms_now);
+    });
     tm.mark("run: iterations");
     const RunCtl c = R.read_ctl();
     RunRecords out;
@@ -391,12 +420,14 @@ class Nonblind final : public NonblindGpu {
     out.diverged_at = c.diverged;
     std::vector<double> rec(2 * static_cast<size_t>(out.iterations));
     if (out.iterations)
-      PDD_CUDA(cudaMemcpy(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost));
+      PDD_CUDA(cudaMemcpyAsync(rec.data(), R.rec.get(), sizeof(double) * rec.size(), cudaMemcpyDeviceToHost, R.st()));
+      PDD_CUDA(cudaStreamSynchronize(R.st()));
     for (int64_t n = 0; n < out.iterations; ++n) {
       out.rf.push_back(rec[2 * n]);
       out.re.push_back(rec[2 * n + 1]);
       out.t_ms.push_back(ms.empty() ? 0.0 : ms[std::min<size_t>(n / 2, ms.size() - 1)] / 2.0);
     }
+    feed.upto(R.rec.template as<double>(), R.rec_cap, R.st(), out.iterations, ms);
     iter_ = out.iterations;
     z_valid_ = false;
     last_lag_.clear();
@@ -467,8 +498,9 @@ class Nonblind final : public NonblindGpu {
     const RunCtl c = R.read_ctl();
     if (c.iter < 1) return NAN;
     double rf = NAN;
-    PDD_CUDA(cudaMemcpy(&rf, R.rec.template as<double>() + 2 * ((c.iter - 1) % R.rec_cap), sizeof(double),
-                        cudaMemcpyDeviceToHost));
+    PDD_CUDA(cudaMemcpyAsync(&rf, R.rec.template as<double>() + 2 * ((c.iter - 1) % R.rec_cap), sizeof(double),
+                             cudaMemcpyDeviceToHost, R.st()));
+    PDD_CUDA(cudaStreamSynchronize(R.st()));
     return rf;
   }
 
@@ -515,11 +547,13 @@ class Nonblind final : public NonblindGpu {
     R.merge_to_host(plan_, U(iter_), out, bp_.get(), bp_.bytes());
   }
   void sync() override { R.stream.sync(); }
+  void* stream() const override { return R.st(); }
   int64_t kernel_launches_per_iteration() const override { return 10; }
 
  private:
   Plan plan_;
   NonblindConfig cfg_;
+  PoolUser pool_;  // before every DevMem: the pool outlives them
   RankData<T> R;
   StateLayout layout_;
   DevMem probe_, probe64_, gamma_[2], bp_, u_[2], v_[2], lam_[2], s_, denom_, z_;
@@ -527,6 +561,7 @@ class Nonblind final : public NonblindGpu {
   std::vector<double> last_lag_;
   Graph full_[2], tail_[2], one_[2];
   int64_t iter_ = 0;
+  int64_t delivered_ = 0;  // run_recording: records handed to the callback
   bool z_valid_ = false;
 };
 

@@ -85,7 +85,8 @@ struct FrameOp {
   Plan plan;
   Layout L;
   Stream stream;
-  DevMem tw, fr_off, fr_pitch, fr_r, fr_c, fr_sub, tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg;
+  AllocStream scope{stream.get()};  // temporaries of the op are ordered on its stream
+  DevMem tw, fr_off, fr_pitch, fr_r, fr_c, fr_sub, tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg, scratch;
   int S;
   FrameOp(int64_t s, int64_t H, int64_t W, const int64_t* pos, int64_t J)
       : plan(single_plan(s, H, W, pos, J)), L(Layout::build(plan, 0, 1)), S(static_cast<int>(s)) {
@@ -105,6 +106,7 @@ struct FrameOp {
     sub_w = upload(L.sub_w, st);
     std::vector<int32_t> pb(2, 0);
     sub_pbeg = upload(pb, st);
+    if (const size_t b = stream_scratch_bytes<T>(S)) scratch.alloc(b, st);
   }
   FrameArgs<T> fargs() const {
     FrameArgs<T> a;
@@ -113,6 +115,7 @@ struct FrameOp {
     a.off = fr_off.as<int64_t>();
     a.pitch = fr_pitch.as<int32_t>();
     a.scale = static_cast<T>(1.0 / static_cast<double>(S));
+    a.scratch = scratch.as<cx<T>>();
     return a;
   }
   template <typename U>
@@ -272,6 +275,7 @@ void op_fft2(double* data, int64_t h, int64_t w, bool inverse) {
   if (h < 1 || w < 1) throw InvalidArgument("ComplexField2D: height, width must be >= 1");
   if (h != w || !frame_supported<T>(static_cast<int>(h))) {
     Stream s;
+    AllocStream scope(s.get());
     generic_fft2<T>(data, h, w, inverse, s.get());
     return;
   }
@@ -425,6 +429,7 @@ void op_prox(const double* y, const double* b, int64_t n, double lambda, double 
   if (!(eps > 0.0 && eps < 1.0)) throw InvalidArgument("stagm: epsilon must lie in (0,1)");
   if (lambda <= 0.0) throw InvalidArgument("stagm::prox: lambda must be positive");
   Stream s;
+  AllocStream scope(s.get());
   cudaStream_t st = s.get();
   DevMem dy = up_doubles<T>(y, 2 * n, st), db = up_doubles<T>(b, n, st), dz(sizeof(double) * 2 * std::max<int64_t>(n, 1));
   prox_kernel<T><<<grid_for(n), 256, 0, st>>>(dy.as<double>(), db.as<double>(), n, static_cast<T>(lambda),
@@ -438,6 +443,7 @@ template <typename T>
 void op_value_gradient(const double* x, const double* b, int64_t n, double eps, double* val, double* grad) {
   if (!(eps > 0.0 && eps < 1.0)) throw InvalidArgument("stagm: epsilon must lie in (0,1)");
   Stream s;
+  AllocStream scope(s.get());
   cudaStream_t st = s.get();
   DevMem dx = up_doubles<T>(x, 2 * n, st), db = up_doubles<T>(b, n, st);
   DevMem dv(sizeof(double) * std::max<int64_t>(n, 1)), dg(sizeof(double) * 2 * std::max<int64_t>(n, 1));
@@ -452,6 +458,7 @@ void op_value_gradient(const double* x, const double* b, int64_t n, double eps, 
 template <typename T>
 void op_intensity(const double* z, int64_t n, double* out) {
   Stream s;
+  AllocStream scope(s.get());
   cudaStream_t st = s.get();
   DevMem dz = up_doubles<T>(z, 2 * n, st), di(sizeof(double) * std::max<int64_t>(n, 1));
   intensity_kernel<T><<<grid_for(n), 256, 0, st>>>(dz.as<double>(), n, di.as<double>());
@@ -463,6 +470,7 @@ void op_intensity(const double* z, int64_t n, double* out) {
 template <typename T>
 void op_diff_norm(const double* cur, const double* prev, int64_t n, double* diff, double* norm) {
   Stream s;
+  AllocStream scope(s.get());
   cudaStream_t st = s.get();
   DevMem a = up_doubles<T>(cur, 2 * n, st), b = up_doubles<T>(prev, 2 * n, st);
   const int nb = static_cast<int>(std::min<int64_t>(std::max<int64_t>((n + 255) / 256, 1), 256));
@@ -484,6 +492,7 @@ void op_diff_norm(const double* cur, const double* prev, int64_t n, double* diff
 template <typename T>
 double op_r_factor(const Plan& plan, const double* subs, const double* intensities, const double* probe) {
   RankData<T> R;
+  AllocStream scope(R.st());
   DataSpec data{intensities, kIntensityF64, false};
   R.build(plan, data, nullptr, 0, nullptr, 1, "r_factor");
   if (R.l1 <= 0.0) throw InvalidArgument("r_factor: all-zero data, metric undefined");

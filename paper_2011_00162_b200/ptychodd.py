@@ -571,6 +571,10 @@ class _DataArg:
             else:
                 self.arr, self.kind = a.to(torch.float64).contiguous(), L.DATA_AMPLITUDE_F64
             self.shape = tuple(a.shape)
+            # the solver copies on its own stream, which is not ordered after
+            # torch's: the producer (and the conversions above) must be done
+            # (ptychodd_cuda.h ordering contract for data_on_device)
+            torch.cuda.current_stream(a.device).synchronize()
         else:
             if frames is not None:
                 self.arr, self.kind = f64(frames), L.DATA_INTENSITY_F64
@@ -649,6 +653,29 @@ class _SolverBase:
         return c128(np.concatenate([c128(a).ravel() for a in arrs]))
 
 
+_RECORD_CB = C.CFUNCTYPE(None, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_double, C.c_void_p)
+
+
+def _record_callback(on_iteration, n_sub):
+    """ctypes trampoline for pdd_*_run_cb: on_iteration(ConvergenceRecord) per
+    iteration while the device loop runs (solver.hpp:88).  Exceptions raised by
+    the callback are collected and re-raised after the run."""
+    errors = []
+    if on_iteration is None:
+        return _RECORD_CB(0), errors
+
+    def tramp(it, rf, re, t_ms, lag, _user):
+        if errors:
+            return
+        try:
+            on_iteration(ConvergenceRecord(int(it), float(rf), float(re), None if math.isnan(lag) else float(lag),
+                                           [float(t_ms)] * n_sub, float(t_ms), float(t_ms)))
+        except BaseException as e:  # noqa: BLE001 - re-raised by the caller
+            errors.append(e)
+
+    return _RECORD_CB(tramp), errors
+
+
 class NonblindSolver(_SolverBase):
     """solver.hpp:72-107 on the GPU.
 
@@ -659,7 +686,8 @@ class NonblindSolver(_SolverBase):
 
     def __init__(self, plan: DecompositionPlan, frames=None, probe=None, config: Optional[NonblindConfig] = None,
                  pin_ones: Optional[np.ndarray] = None, *, amplitudes=None, dtype=None, device: int = 0,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 devices: Optional[Sequence[int]] = None):
         self.plan, self.config = plan, config or NonblindConfig()
         g = plan.geometry
         self._data = _DataArg(frames, amplitudes)
@@ -674,7 +702,12 @@ class NonblindSolver(_SolverBase):
         self.device, self.rank, self.world = device, rank, world
         self._cfg = self.config.c()
         h = C.c_void_p()
-        if world > 1 or nccl_id is not None:
+        if devices is not None:  # one handle over len(devices) in-process ranks
+            devs = (C.c_int32 * len(devices))(*devices)
+            check(L.lib().pdd_nonblind_create_multi(plan.handle, ptr(self._data.arr), self._data.kind,
+                                                    int(self._data.on_device), ptr(self.probe), C.byref(self._cfg),
+                                                    ptr(self._pin), self.dtype, devs, len(devices), C.byref(h)))
+        elif world > 1 or nccl_id is not None:
             idb = C.create_string_buffer(bytes(nccl_id), 128)
             check(L.lib().pdd_nonblind_create_rank(plan.handle, ptr(self._data.arr), self._data.kind,
                                                    int(self._data.on_device), ptr(self.probe), C.byref(self._cfg),
@@ -756,8 +789,9 @@ class NonblindSolver(_SolverBase):
         return num / self._sqrt_f_l1
 
     def run(self, on_iteration: Optional[Callable[[ConvergenceRecord], None]] = None) -> NonblindResult:
-        """solver.cpp:216-267 (performance path: no per-iteration host round trip;
-        records are delivered to on_iteration after the device loop)."""
+        """solver.cpp:216-267 (performance path: no per-iteration host round
+        trip; on_iteration receives each record while the device loop runs, at
+        most one poll window behind it)."""
         cfg = self.config
         n = C.c_int64()
         div = C.c_int64()
@@ -765,9 +799,12 @@ class NonblindSolver(_SolverBase):
         g = self.plan.geometry
         pf = _Prefault((g.image_height, g.image_width) if self.world == 1 else (0,), (self._lay.image_elems,))
         pf.start()
-        rc = L.lib().pdd_nonblind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
+        cb, errors = _record_callback(on_iteration, len(self.local_subs))
+        rc = L.lib().pdd_nonblind_run_cb(self._h, cb, None, C.byref(n), ptr(rec), C.byref(div))
         merged, u = pf.result()
         check(rc, iteration=int(div.value))
+        if errors:
+            raise errors[0]
         lag = [None] * int(n.value)
         if cfg.record_lagrangian:  # solver.cpp:258-260, evaluated on the device
             nl = C.c_int64()
@@ -779,8 +816,6 @@ class NonblindSolver(_SolverBase):
             r = ConvergenceRecord(k + 1, float(rec[k, 0]), float(rec[k, 1]), lag[k],
                                   [float(rec[k, 2])] * len(self.local_subs), float(rec[k, 2]), float(rec[k, 2]))
             records.append(r)
-            if on_iteration:
-                on_iteration(r)
         if self.world == 1:  # merged on the device (ddplan.cpp:104-121)
             check(L.lib().pdd_nonblind_merged(self._h, ptr(merged)))
         else:
@@ -898,7 +933,8 @@ class BlindSolver(_SolverBase):
 
     def __init__(self, plan: DecompositionPlan, frames=None, config: Optional[BlindConfig] = None,
                  pin_ones: Optional[np.ndarray] = None, *, amplitudes=None, dtype=None, device: int = 0,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                 devices: Optional[Sequence[int]] = None):
         self.plan, self.config = plan, config or BlindConfig()
         g = plan.geometry
         s = g.frame_side
@@ -915,7 +951,12 @@ class BlindSolver(_SolverBase):
         self.device, self.rank, self.world = device, rank, world
         self._cfg = self.config.c()
         h = C.c_void_p()
-        if world > 1 or nccl_id is not None:
+        if devices is not None:
+            devs = (C.c_int32 * len(devices))(*devices)
+            check(L.lib().pdd_blind_create_multi(plan.handle, ptr(self._data.arr), self._data.kind,
+                                                 int(self._data.on_device), C.byref(self._cfg), ptr(self._mask),
+                                                 ptr(self._pin), self.dtype, devs, len(devices), C.byref(h)))
+        elif world > 1 or nccl_id is not None:
             idb = C.create_string_buffer(bytes(nccl_id), 128)
             check(L.lib().pdd_blind_create_rank(plan.handle, ptr(self._data.arr), self._data.kind,
                                                 int(self._data.on_device), C.byref(self._cfg), ptr(self._mask),
@@ -1000,16 +1041,17 @@ class BlindSolver(_SolverBase):
         g = self.plan.geometry
         pf = _Prefault((g.image_height, g.image_width) if self.world == 1 else (0,), (self._lay.image_elems,))
         pf.start()
-        rc = L.lib().pdd_blind_run(self._h, C.byref(n), ptr(rec), C.byref(div))
+        cb, errors = _record_callback(on_iteration, len(self.local_subs))
+        rc = L.lib().pdd_blind_run_cb(self._h, cb, None, C.byref(n), ptr(rec), C.byref(div))
         merged, u = pf.result()
         check(rc, iteration=int(div.value))
+        if errors:
+            raise errors[0]
         records = []
         for k in range(int(n.value)):
             r = ConvergenceRecord(k + 1, float(rec[k, 0]), float(rec[k, 1]), None,
                                   [float(rec[k, 2])] * len(self.local_subs), float(rec[k, 2]), float(rec[k, 2]))
             records.append(r)
-            if on_iteration:
-                on_iteration(r)
         check(L.lib().pdd_blind_get_state(self._h, None, None, None, ptr(u), None, None, None, None, None))
         u = self._split_images(u)
         probe, spec, mask, _ = self._probe_info()

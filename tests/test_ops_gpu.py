@@ -25,8 +25,6 @@ def rfield(shape, seed):
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("s", [2, 4, 8, 16, 32, 64, 128])
 def test_fft2_matches_numpy(dtype, s):
-    if dtype == "f64" and s == 128:
-        pytest.skip("float64 frames are supported up to 64")
     x = rfield((s, s), s)
     assert rel_l2(P.fft2_normalized(x, dtype=dtype), O.fft2n(x)) < TOL[dtype]
     assert rel_l2(P.ifft2_normalized(x, dtype=dtype), O.ifft2n(x)) < TOL[dtype]
@@ -52,8 +50,6 @@ def test_fft_dc_known_answer():
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 @pytest.mark.parametrize("H,s,step", [(12, 4, 2), (40, 8, 4), (128, 32, 8), (256, 64, 16), (384, 128, 32)])
 def test_forward_adjoint_density(dtype, H, s, step):
-    if dtype == "f64" and s == 128:
-        pytest.skip("float64 frames are supported up to 64")
     g = O.make_raster_scan(H, H, s, step)
     gp = P.make_raster_scan(H, H, s, step)
     probe, img = rfield((s, s), 1), rfield((H, H), 2)

@@ -15,13 +15,17 @@
 //
 // The solver objects stay host-only (the reference classes have no slot for a
 // device handle): each entry point opens a device handle, works, and closes
-// it.  run() is one handle for the whole solve; step() round-trips the state
+// it.  The handle spans min(threads or D, D, visible GPUs) devices
+// (devices_for); run() streams on_iteration records while the device loop
+// runs.  run() is one handle for the whole solve; step() round-trips the state
 // (the correctness path, as in the reference's API).  Precision: float64 by
 // default (the reference's), PTYCHODD_CUDA_DTYPE=f32 selects complex64.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <string>
 
@@ -43,6 +47,61 @@ int device() {
   const char* e = std::getenv("PTYCHODD_CUDA_DEVICE");
   return e ? std::atoi(e) : 0;
 }
+
+// The reference's worker count (NonblindConfig::threads / BlindConfig::threads,
+// 0 = one worker per subdomain, solver.cpp:122) mapped onto GPUs: G =
+// min(threads or D, D, visible devices) ranks on consecutive devices from
+// PTYCHODD_CUDA_DEVICE.  PTYCHODD_CUDA_DEVICES="0,0,..." lists them explicitly
+// (a repeated device runs several ranks on one GPU through the host
+// transport).  Results do not depend on G (bit-identical iterates).
+std::vector<int32_t> devices_for(int threads, int D) {
+  std::vector<int32_t> out;
+  if (const char* e = std::getenv("PTYCHODD_CUDA_DEVICES")) {
+    std::string l(e);
+    size_t a = 0;
+    while (a < l.size()) {
+      const size_t b = l.find(',', a);
+      out.push_back(std::atoi(l.substr(a, b == std::string::npos ? std::string::npos : b - a).c_str()));
+      if (b == std::string::npos) break;
+      a = b + 1;
+    }
+    if (static_cast<int>(out.size()) > D) out.resize(static_cast<size_t>(D));
+    if (!out.empty()) return out;
+  }
+  int32_t n = 0;
+  if (pdd_device_count(&n) != PDD_OK || n < 1) n = 1;
+  const int base = device();
+  int G = threads > 0 ? threads : D;
+  G = std::max(1, std::min({G, D, n - std::min(base, n - 1)}));
+  for (int r = 0; r < G; ++r) out.push_back(base + r);
+  return out;
+}
+
+// run()'s per-iteration callback (solver.hpp:88) through pdd_*_run_cb: the
+// C-ABI streams records while the device loop runs; an exception thrown by
+// the caller's callback is held and rethrown once the run returns.
+struct RecordTrampoline {
+  const std::function<void(const ConvergenceRecord&)>* cb;
+  int D;
+  std::exception_ptr err;
+  static void call(int64_t it, double rf, double re, double t_ms, double lag, void* user) {
+    auto* self = static_cast<RecordTrampoline*>(user);
+    if (self->err || !self->cb || !*self->cb) return;
+    ConvergenceRecord r;
+    r.iteration = it;
+    r.rf = rf;
+    r.re = re;
+    if (!std::isnan(lag)) r.lagrangian = lag;
+    r.t_sub_ms.assign(static_cast<size_t>(self->D), t_ms);
+    r.t_virtual_ms = t_ms;
+    r.t_actual_ms = t_ms;
+    try {
+      (*self->cb)(r);
+    } catch (...) {
+      self->err = std::current_exception();
+    }
+  }
+};
 
 // C-ABI status -> the reference's exception types (DivergenceError included).
 void check(int rc, int64_t iteration = 0) {
@@ -239,8 +298,13 @@ struct NbHandle {
     const auto f = global_frames(frames, p);
     const auto pin = global_pins(p, pins);
     const auto c = c_config(cfg);
-    check(pdd_nonblind_create(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, dp(probe.data()), &c, pin.data(), dtype(),
-                              device(), &h));
+    const auto devs = devices_for(cfg.threads, p.D);
+    if (devs.size() == 1)
+      check(pdd_nonblind_create(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, dp(probe.data()), &c, pin.data(),
+                                dtype(), devs[0], &h));
+    else
+      check(pdd_nonblind_create_multi(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, dp(probe.data()), &c, pin.data(),
+                                      dtype(), devs.data(), static_cast<int32_t>(devs.size()), &h));
   }
   ~NbHandle() { pdd_nonblind_destroy(h); }
 };
@@ -254,8 +318,13 @@ struct BlHandle {
     const auto pin = global_pins(p, pins);
     const auto c = c_config(cfg);
     const double* mask = cfg.support_mask.size() > 0 ? cfg.support_mask.data().data() : nullptr;
-    check(pdd_blind_create(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, &c, mask, pin.data(), dtype(), device(),
-                           &h));
+    const auto devs = devices_for(cfg.threads, p.D);
+    if (devs.size() == 1)
+      check(pdd_blind_create(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, &c, mask, pin.data(), dtype(), devs[0],
+                             &h));
+    else
+      check(pdd_blind_create_multi(plan->h, f.data(), PDD_DATA_INTENSITY_F64, 0, &c, mask, pin.data(), dtype(),
+                                   devs.data(), static_cast<int32_t>(devs.size()), &h));
   }
   ~BlHandle() { pdd_blind_destroy(h); }
 };
@@ -360,7 +429,9 @@ NonblindResult NonblindSolver::run(const std::function<void(const ConvergenceRec
   NbHandle g(plan_, frames_, probe_, config_, pin_);
   std::vector<double> rec(3 * static_cast<size_t>(config_.max_iters));
   int64_t n = 0, div = 0;
-  check(pdd_nonblind_run(g.h, &n, rec.data(), &div), div);
+  RecordTrampoline tr{&on_iteration, plan_.D, nullptr};
+  check(pdd_nonblind_run_cb(g.h, on_iteration ? &RecordTrampoline::call : nullptr, &tr, &n, rec.data(), &div), div);
+  if (tr.err) std::rethrow_exception(tr.err);
   std::vector<double> lag;
   if (config_.record_lagrangian) {
     int64_t nl = 0;
@@ -370,8 +441,6 @@ NonblindResult NonblindSolver::run(const std::function<void(const ConvergenceRec
   }
   NonblindResult out;
   out.records = records_of(rec, n, plan_.D, lag);
-  if (on_iteration)
-    for (const auto& r : out.records) on_iteration(r);
   Packed p = sized(plan_);
   check(pdd_nonblind_get_state(g.h, dp(p.u), nullptr, nullptr, nullptr, nullptr, nullptr));
   out.sub_solutions = split_images(plan_, p.u);
@@ -496,11 +565,11 @@ BlindResult BlindSolver::run(const std::function<void(const ConvergenceRecord&)>
   check(pdd_blind_init_state(g.h, nullptr));  // the device solver's own w0 (== w0_)
   std::vector<double> rec(3 * static_cast<size_t>(config_.max_iters));
   int64_t n = 0, div = 0;
-  check(pdd_blind_run(g.h, &n, rec.data(), &div), div);
+  RecordTrampoline tr{&on_iteration, plan_.D, nullptr};
+  check(pdd_blind_run_cb(g.h, on_iteration ? &RecordTrampoline::call : nullptr, &tr, &n, rec.data(), &div), div);
+  if (tr.err) std::rethrow_exception(tr.err);
   BlindResult out;
   out.records = records_of(rec, n, plan_.D, {});
-  if (on_iteration)
-    for (const auto& r : out.records) on_iteration(r);
   const int64_t s = plan_.geometry.frame_side;
   out.probe = ComplexField2D(s, s);
   out.probe_fourier = ComplexField2D(s, s);

@@ -36,6 +36,23 @@ def test_reference_unit_tests_pass_on_the_gpu_library():
     assert "blind recovery on a toy problem drives RF down with exact support zeros" in ok
 
 
+@pytest.mark.skipif(not os.path.exists(BIN), reason="drop-in test binary not built (needs /root/reference)")
+def test_reference_unit_tests_pass_with_multi_rank_handles():
+    """The same 53 reference test cases with every solver handle spanning up to
+    three in-process ranks (NonblindConfig::threads -> GPUs,
+    dropin/ptychodd_solver_cuda.cpp devices_for): PTYCHODD_CUDA_DEVICES=0,0,0
+    puts the ranks on this box's one GPU (host transport), so the cut-pair
+    exchange, the all-reduces and the state assembly of the multi-rank handle
+    run under the reference's own assertions (incl. the 1e-12 transparent-ADMM
+    equivalence and the thread-count determinism case)."""
+    env = dict(os.environ, PTYCHODD_CUDA_DEVICES="0,0,0")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=900, env=env)
+    ok = set(re.findall(r"^\[  OK  \] (.*)$", r.stderr, re.M))
+    failed = set(re.findall(r"^\[ FAIL \] (.*)$", r.stderr, re.M))
+    assert not failed, r.stderr[-4000:]
+    assert len(ok) == 53 and r.returncode == 0, r.stdout + r.stderr[-2000:]
+
+
 ACC = os.path.join(ROOT, "dropin", "_build", "ptychodd_dropin_acceptance")
 
 

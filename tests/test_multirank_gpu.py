@@ -99,3 +99,26 @@ def test_more_ranks_than_subdomains_is_rejected():
     plan, f, probe = problem(D=2)
     with pytest.raises(P.InvalidArgument):
         P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f32", devices=[0, 0, 0])
+
+
+def test_on_iteration_streams_records_during_the_run():
+    """solver.hpp:88: on_iteration sees every record, in order, while the device
+    loop runs (poll windows of 16 iterations), not after it returns."""
+    import time
+
+    plan, f, probe = problem(N=512, s=64, step=16, D=2)
+    cfg = P.NonblindConfig(max_iters=1500, tol_rf=1e-300)
+    sol = P.NonblindSolver(plan, f, probe, cfg, dtype="f32")
+    seen = []
+    res = sol.run(on_iteration=lambda r: seen.append((time.perf_counter(), r)))
+    t_ret = time.perf_counter()
+    assert [r.iteration for _, r in seen] == list(range(1, res.iterations + 1))
+    assert [r.rf for _, r in seen] == [r.rf for r in res.records]
+    assert [r.re for _, r in seen] == [r.re for r in res.records]
+    first, last = seen[0][0], seen[-1][0]
+    assert last - first > 0.5 * (t_ret - first)  # spread over the loop, not delivered at the end
+    # multi-rank handles stream from rank 0
+    seen2 = []
+    P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=40, tol_rf=1e-300), dtype="f32",
+                     devices=[0, 0]).run(on_iteration=seen2.append)
+    assert [r.iteration for r in seen2] == list(range(1, 41))

@@ -318,8 +318,9 @@ def solver_for(cfg, plan, probe, data, iters, local, rank, world, nccl_id, inten
     key = "frames" if intensities else "amplitudes"
     if cfg.blind:
         bc = P.BlindConfig(max_iters=iters, tol_rf=1e-300, **cfg.solver)
-        return P.BlindSolver(plan, None, bc, **{key: data}, **kw)
-    return P.NonblindSolver(plan, None, probe, P.NonblindConfig(max_iters=iters, tol_rf=1e-300), **{key: data}, **kw)
+        return P.BlindSolver(plan, config=bc, **{key: data}, **kw)
+    return P.NonblindSolver(plan, probe=probe, config=P.NonblindConfig(max_iters=iters, tol_rf=1e-300),
+                            **{key: data}, **kw)
 
 
 def e2e_solve(cfg, plan, probe, data, local, rank, world, nccl_id, dist, intensities=False, w0=None):

@@ -7,7 +7,8 @@
  *   PDD_OK 0, PDD_INVALID_ARGUMENT 1 (std::invalid_argument),
  *   PDD_OUT_OF_RANGE 2 (std::out_of_range), PDD_RUNTIME_ERROR 3
  *   (std::runtime_error), PDD_DIVERGENCE 4 (ptychodd::DivergenceError,
- *   solver.hpp:62-68; iteration index via the out-parameter), PDD_CUDA_ERROR 5
+ *   solver.hpp:62-68; iteration index via the out-parameter), PDD_CUDA_ERROR 5,
+ *   PDD_FORMAT_ERROR 6 (ptychodd::FormatError, io.hpp:12-18)
  * and pdd_last_error() returns the thread-local message.  A C++ or Python shim
  * rethrows the reference's exception types from these codes.
  *
@@ -42,12 +43,20 @@ enum {
   PDD_OUT_OF_RANGE = 2,
   PDD_RUNTIME_ERROR = 3,
   PDD_DIVERGENCE = 4,
-  PDD_CUDA_ERROR = 5
+  PDD_CUDA_ERROR = 5,
+  PDD_FORMAT_ERROR = 6 /* ptychodd::FormatError (io.hpp:12-18): malformed PTYA input */
 };
 enum { PDD_F32 = 1, PDD_F64 = 2 };
 enum { PDD_AXIS_AUTO = 0, PDD_AXIS_COLUMNS = 1, PDD_AXIS_ROWS = 2 }; /* ddplan.hpp:7 SplitAxis */
 enum { PDD_STOP_RFACTOR = 0, PDD_STOP_RELATIVE_ERROR = 1 };           /* solver.hpp:11-14 StopRule */
-enum { PDD_DATA_INTENSITY_F64 = 0, PDD_DATA_AMPLITUDE_F32 = 1, PDD_DATA_AMPLITUDE_F64 = 2 };
+/* Measured data handed to the solver constructors: a [J][s][s] array in global
+ * scan order, or (PDD_DATA_PTYA_FRAMES_F64, host only) `data` is the
+ * NUL-terminated path of a frames.ptya stack of float64 intensities -- the
+ * file the reference's CLI loads with read_frames (io.cpp:186-202) -- streamed
+ * from disk through page-locked chunks to the device, where it is converted to
+ * amplitudes; validated like read_frames + FrameStack::validate. */
+enum { PDD_DATA_INTENSITY_F64 = 0, PDD_DATA_AMPLITUDE_F32 = 1, PDD_DATA_AMPLITUDE_F64 = 2,
+       PDD_DATA_PTYA_FRAMES_F64 = 3 };
 
 PDD_API const char* pdd_last_error(void);
 PDD_API int pdd_version(void);
@@ -162,6 +171,11 @@ PDD_API int pdd_nonblind_create_multi(const pdd_plan* plan, const void* data, in
                                       int32_t data_on_device, const double* probe, const pdd_nonblind_config* cfg,
                                       const double* pin_ones, int32_t dtype, const int32_t* devices,
                                       int32_t n_devices, pdd_nonblind** out);
+/* PTYA header (io.cpp:80-115): dtype code to expect (1 f64, 2 c128), ndim,
+ * dims (up to 4, zero-padded), payload byte offset.  PDD_FORMAT_ERROR with the
+ * byte offset in the message on malformed input. */
+PDD_API int pdd_ptya_header(const char* path, int32_t want_dtype, int32_t* ndim, int64_t* dims4,
+                            int64_t* payload_offset);
 /* A 128-byte id for the in-process host transport, usable in place of an NCCL
  * id by pdd_*_create_rank when the ranks are threads of one process (tests of
  * the rank-sharded path on one device).  No reference counterpart. */
@@ -283,10 +297,12 @@ PDD_API int pdd_host_free(void* p);
  * values already). */
 PDD_API int pdd_host_stage_reserve(void);
 /* Device memory is drawn from a library-private stream-ordered pool per device
- * that keeps freed blocks mapped while any solver lives on that device (the
- * pool is trimmed when the last one is destroyed).  This returns every unused
- * block of every pool to the driver now (synchronises the devices used).  No
- * reference counterpart. */
+ * whose freed blocks stay mapped for the next solver (repeated solves skip the
+ * page mapping of multi-GB buffers); the device's default pool and other
+ * allocators in the process are untouched.  This returns every unused block
+ * of every pool to the driver now (synchronises the devices used); with
+ * PDD_POOL_TRIM_ON_IDLE=1 it happens automatically when the last solver on a
+ * device is destroyed.  No reference counterpart. */
 PDD_API int pdd_release_cached_memory(void);
 
 #ifdef __cplusplus

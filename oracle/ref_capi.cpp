@@ -29,6 +29,9 @@
 #include "ptychodd/ddplan.hpp"
 #include "ptychodd/fft.hpp"
 #include "ptychodd/forward.hpp"
+#ifdef REF_HAVE_IO
+#include "ptychodd/io.hpp"
+#endif
 #include "ptychodd/metrics.hpp"
 #include "ptychodd/simulate.hpp"
 #include "ptychodd/solver.hpp"
@@ -562,5 +565,81 @@ double ref_r_factor_subs(const RefPlanSpec* ps, const double* subs, const double
   });
   return out;
 }
+
+#ifdef REF_HAVE_IO
+// ---- the reference's own I/O (io.cpp): PTYA files and dataset directories ----
+// A dataset directory as cmd_simulate writes it (ptychodd_cli.cpp:155-169):
+// frames.ptya, probe.ptya, optional pin.ptya / sample.ptya, meta.json with
+// schema_version 1, kind "dataset", the geometry record and a noise record
+// (null: noiseless).  Raster geometry from make_raster_scan(H, W, s, step).
+int ref_write_dataset(const char* dir, int64_t H, int64_t W, int64_t s, int64_t step, const double* frames,
+                      const double* probe, const double* pin, const double* sample, int noisy) {
+  return guard([&] {
+    const std::filesystem::path out(dir);
+    std::filesystem::create_directories(out);
+    const ScanGeometry g = make_raster_scan(H, W, s, step);
+    std::vector<RealField2D> fr;
+    for (int64_t j = 0; j < g.frame_count(); ++j) fr.push_back(rfield(frames + s * s * j, s, s));
+    write_frames(out / "frames.ptya", fr);
+    write_array(out / "probe.ptya", cfield(probe, s, s));
+    if (pin) write_array(out / "pin.ptya", rfield(pin, H, W));
+    if (sample) write_array(out / "sample.ptya", cfield(sample, H, W));
+    nlohmann::json noise = nullptr;
+    if (noisy) noise = {{"target_snr_db", 30.0}};
+    nlohmann::json meta = {{"schema_version", 1}, {"kind", "dataset"}, {"geometry", geometry_to_json(g)},
+                           {"seed", 1}, {"border", 0}, {"noise", noise}};
+    write_json(out / "meta.json", meta);
+  });
+}
+
+int ref_write_frames(const char* path, const double* frames, int64_t J, int64_t h, int64_t w) {
+  return guard([&] {
+    std::vector<RealField2D> fr;
+    for (int64_t j = 0; j < J; ++j) fr.push_back(rfield(frames + h * w * j, h, w));
+    write_frames(path, fr);
+  });
+}
+
+int ref_write_complex(const char* path, const double* data, int64_t h, int64_t w) {
+  return guard([&] { write_array(path, cfield(data, h, w)); });
+}
+
+int ref_write_real(const char* path, const double* data, int64_t h, int64_t w) {
+  return guard([&] { write_array(path, rfield(data, h, w)); });
+}
+
+// read_complex_array / read_real_array / read_frames: dims first (out may be
+// NULL), then the payload.  FormatError -> 6.
+int ref_read_array(const char* path, int kind, int64_t* dims3, double* out) {
+  try {
+    if (kind == 2) {
+      const ComplexField2D f = read_complex_array(path);
+      dims3[0] = f.height();
+      dims3[1] = f.width();
+      dims3[2] = 1;
+      if (out) put(out, f);
+    } else if (kind == 1) {
+      const RealField2D f = read_real_array(path);
+      dims3[0] = f.height();
+      dims3[1] = f.width();
+      dims3[2] = 1;
+      if (out) put(out, f);
+    } else {
+      const auto fr = read_frames(path);
+      dims3[0] = static_cast<int64_t>(fr.size());
+      dims3[1] = fr.empty() ? 0 : fr[0].height();
+      dims3[2] = fr.empty() ? 0 : fr[0].width();
+      if (out)
+        for (const auto& f : fr) out = put(out, f);
+    }
+    return 0;
+  } catch (const FormatError& e) {
+    return fail(e, 6);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
+#endif  // REF_HAVE_IO
 
 }  // extern "C"

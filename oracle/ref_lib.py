@@ -326,3 +326,41 @@ def toy(size, probe_side, step, seed):
     _check(lib().ref_toy(C.c_int64(size), C.c_int64(probe_side), C.c_int64(step), C.c_uint64(seed),
                          _p(sample), _p(probe), _p(pin)))
     return sample, probe, pin
+
+
+# ---- the reference's own I/O (io.cpp), when compiled in (build_ref.sh) ----
+def has_io() -> bool:
+    return available() and hasattr(lib(), "ref_write_dataset")
+
+
+def write_dataset(path, H, W, s, step, frames, probe, pin=None, sample=None, noisy=False) -> None:
+    """A dataset directory exactly as the reference CLI's `simulate` writes it
+    (ptychodd_cli.cpp:155-169): frames.ptya, probe.ptya, [pin.ptya],
+    [sample.ptya], meta.json."""
+    pin = None if pin is None else _d(pin)
+    sample = None if sample is None else _c(sample)
+    _check(lib().ref_write_dataset(os.fsencode(str(path)), C.c_int64(H), C.c_int64(W), C.c_int64(s),
+                                   C.c_int64(step), _p(_d(frames)), _p(_c(probe)), _p(pin), _p(sample),
+                                   C.c_int(int(noisy))))
+
+
+def write_frames(path, frames) -> None:
+    f = _d(frames)
+    _check(lib().ref_write_frames(os.fsencode(str(path)), _p(f), C.c_int64(f.shape[0]), C.c_int64(f.shape[1]),
+                                  C.c_int64(f.shape[2])))
+
+
+def read_array(path, kind: str):
+    """kind 'complex' | 'real' | 'frames' -> numpy array via read_complex_array /
+    read_real_array / read_frames.  FormatError surfaces as RefError code 6."""
+    code = {"frames": 0, "real": 1, "complex": 2}[kind]
+    dims = np.zeros(3, np.int64)
+    _check(lib().ref_read_array(os.fsencode(str(path)), C.c_int(code), _p(dims), None))
+    if code == 2:
+        out = np.zeros((int(dims[0]), int(dims[1])), np.complex128)
+    elif code == 1:
+        out = np.zeros((int(dims[0]), int(dims[1])))
+    else:
+        out = np.zeros((int(dims[0]), int(dims[1]), int(dims[2])))
+    _check(lib().ref_read_array(os.fsencode(str(path)), C.c_int(code), _p(dims), _p(out)))
+    return out

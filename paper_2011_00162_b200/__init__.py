@@ -2,7 +2,7 @@
 ADMM ptychography iteration as sm_100a CUDA kernels behind a C-ABI
 (include/ptychodd_cuda.h), with a Python mirror of the reference ptychodd API.
 """
-from ._lib import (LIB_PATH, CudaError, DivergenceError, InvalidArgument, OutOfRange, PtychoRuntimeError,
+from ._lib import (LIB_PATH, CudaError, DivergenceError, FormatError, InvalidArgument, OutOfRange, PtychoRuntimeError,
                    exported_symbols, lib)
 from .ptychodd import (BlindConfig, BlindResult, BlindSolver, BlindState, ConvergenceRecord, DecompositionPlan, NonblindConfig, NonblindResult, NonblindSolver, Region,
                        ScanGeometry, SolverState, adjoint, adjoint_probe, fft2_normalized, forward, ifft2_normalized,

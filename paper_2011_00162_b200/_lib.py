@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("PDD_LIB") or os.path.join(os.path.dirname(os.path.abs
                                                     "libptychodd_cuda.so")
 
 PDD_F32, PDD_F64 = 1, 2
-DATA_INTENSITY_F64, DATA_AMPLITUDE_F32, DATA_AMPLITUDE_F64 = 0, 1, 2
+DATA_INTENSITY_F64, DATA_AMPLITUDE_F32, DATA_AMPLITUDE_F64, DATA_PTYA_FRAMES_F64 = 0, 1, 2, 3
 
 
 class InvalidArgument(ValueError):
@@ -40,6 +40,10 @@ class DivergenceError(RuntimeError):
 
 class CudaError(RuntimeError):
     """CUDA / NCCL failure."""
+
+
+class FormatError(RuntimeError):
+    """ptychodd::FormatError (io.hpp:12-18): malformed or truncated PTYA/JSON input."""
 
 
 class PlanInfo(C.Structure):
@@ -92,6 +96,8 @@ def check(rc: int, iteration: int = 0) -> None:
         raise PtychoRuntimeError(msg)
     if rc == 4:
         raise DivergenceError(iteration, msg)
+    if rc == 6:
+        raise FormatError(msg)
     raise CudaError(msg)
 
 
@@ -100,6 +106,8 @@ def ptr(a):
         return None
     if hasattr(a, "data_ptr"):  # torch tensor
         return C.c_void_p(a.data_ptr())
+    if isinstance(a, C.c_char_p):  # a path (PTYA frames)
+        return C.cast(a, C.c_void_p)
     return a.ctypes.data_as(C.c_void_p)
 
 

@@ -296,7 +296,9 @@ class Blind final : public BlindGpu {
     p2.frames_in = spec_.as<cx<T>>();
     p2.bp_out = w_.as<cx<T>>();
     PDD_CUDA(launch_frame<T>(kAdj, R.S, p2, s));
-    // v-step from u^n, Lambda^n
+    // v-step from u^n, Lambda^n (blind.cpp:209-218).  Sequential here: the
+    // blind image-side state is single-buffered (only Gamma ping-pongs), so
+    // the v-step must see this iteration's stop decision (skipB).
     R.consensus(u_.as<cx<T>>(), lam_.as<cx<T>>(), s_.as<cx<T>>(), v_.as<cx<T>>(), R.skipB());
     // W-step with u^n
     PDD_CUDA(launch_probe_partials<T>(u_.as<cx<T>>(), R.fr_off.template as<int64_t>(), R.fr_pitch.template as<int32_t>(),

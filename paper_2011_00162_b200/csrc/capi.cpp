@@ -14,6 +14,7 @@
 #include "layout.hpp"
 #include "ops.hpp"
 #include "plan.hpp"
+#include "ptya.hpp"
 
 struct pdd_plan {
   pdd::Plan plan;
@@ -44,6 +45,9 @@ int guard(F&& f) {
   } catch (const pdd::CudaError& e) {
     g_err = e.what();
     return PDD_CUDA_ERROR;
+  } catch (const pdd::FormatError& e) {
+    g_err = e.what();
+    return PDD_FORMAT_ERROR;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return PDD_INVALID_ARGUMENT;
@@ -477,7 +481,8 @@ static int nonblind_create(const pdd_plan* plan, const void* data, int32_t kind,
     need(data, "data");
     need(probe, "probe");
     need(out, "out");
-    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind < 0 || kind > 3) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind == PDD_DATA_PTYA_FRAMES_F64 && on_dev) throw pdd::InvalidArgument("a PTYA path is host data");
     const bool f64 = is_f64(dtype);
     auto h = std::make_unique<pdd_nonblind>();
     h->device = device;
@@ -517,7 +522,8 @@ int pdd_nonblind_create_multi(const pdd_plan* plan, const void* data, int32_t ki
     need(probe, "probe");
     need(devices, "devices");
     need(out, "out");
-    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind < 0 || kind > 3) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind == PDD_DATA_PTYA_FRAMES_F64 && on_dev) throw pdd::InvalidArgument("a PTYA path is host data");
     if (n_devices < 1) throw pdd::InvalidArgument("n_devices >= 1");
     const bool f64 = is_f64(dtype);
     auto h = std::make_unique<pdd_nonblind>();
@@ -527,6 +533,17 @@ int pdd_nonblind_create_multi(const pdd_plan* plan, const void* data, int32_t ki
     h->s = pdd::make_nonblind_multi(plan->plan, spec, probe, nb_cfg(cfg), pin, f64 ? 2 : 1,
                                     std::vector<int>(devices, devices + n_devices));
     *out = h.release();
+  });
+}
+
+int pdd_ptya_header(const char* path, int32_t want_dtype, int32_t* ndim, int64_t* dims4, int64_t* payload_offset) {
+  return guard([&] {
+    need(path, "path");
+    const pdd::PtyaHeader h = pdd::ptya_read_header(path, static_cast<uint16_t>(want_dtype));
+    if (ndim) *ndim = static_cast<int32_t>(h.dims.size());
+    if (dims4)
+      for (size_t i = 0; i < 4; ++i) dims4[i] = i < h.dims.size() ? static_cast<int64_t>(h.dims[i]) : 0;
+    if (payload_offset) *payload_offset = static_cast<int64_t>(h.payload_offset);
   });
 }
 
@@ -652,7 +669,8 @@ static int blind_create(const pdd_plan* plan, const void* data, int32_t kind, in
     need(plan, "plan");
     need(data, "data");
     need(out, "out");
-    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind < 0 || kind > 3) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind == PDD_DATA_PTYA_FRAMES_F64 && on_dev) throw pdd::InvalidArgument("a PTYA path is host data");
     const bool f64 = is_f64(dtype);
     auto h = std::make_unique<pdd_blind>();
     h->device = device;
@@ -676,7 +694,8 @@ int pdd_blind_create_multi(const pdd_plan* plan, const void* data, int32_t kind,
     need(data, "data");
     need(devices, "devices");
     need(out, "out");
-    if (kind < 0 || kind > 2) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind < 0 || kind > 3) throw pdd::InvalidArgument("data_kind out of range");
+    if (kind == PDD_DATA_PTYA_FRAMES_F64 && on_dev) throw pdd::InvalidArgument("a PTYA path is host data");
     if (n_devices < 1) throw pdd::InvalidArgument("n_devices >= 1");
     const bool f64 = is_f64(dtype);
     auto h = std::make_unique<pdd_blind>();

@@ -22,6 +22,7 @@
 #include "frame_kernel.cuh"
 #include "kernels.hpp"
 #include "layout.hpp"
+#include "ptya.hpp"
 
 namespace pdd {
 
@@ -302,11 +303,14 @@ struct RankData {
   int S = 0, device = 0;
   Comm* comm = nullptr;
   Stream stream;
+  Stream side;  // the forked consensus branch of the iteration (fork_consensus)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   DevMem amp, tw;
   DevMem fr_off, fr_pitch, fr_r, fr_c, fr_sub;
   DevMem tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg, psides, pgeom;
   DevMem sub_fr_beg, sub_tile_beg, local_map;
   DevMem pc_beg, pc_pos, pc_ofs, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
+  DevMem fmeta_beg, fmeta, fmeta_base, imeta_beg, imeta, imeta_base, tps_beg, tps;  // flattened gather lists
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
   DevMem scratch;  // global transpose tiles of the streamed kernel (complex128 128^2 frames)
   DevMem ctl, rec;
@@ -324,6 +328,7 @@ struct RankData {
   RunCtl* ctlp() const { return ctl.as<RunCtl>(); }
   int* skipA() const { return &ctl.as<RunCtl>()->skipA; }
   int* skipB() const { return &ctl.as<RunCtl>()->skipB; }
+  int* skipC() const { return &ctl.as<RunCtl>()->skipC; }
 
   // piece_len > 1: multi-frame back-projection pieces for the streamed sweep (layout.hpp)
   void build(const Plan& plan, const DataSpec& data, const double* pin_ones, int dev, Comm* c, int max_iters,
@@ -370,7 +375,15 @@ struct RankData {
       pc_pos = upload(L.cta_pos, s);
       pc_ofs = upload(L.cta_ofs, s);
     }
+    fmeta_beg = upload(L.fmeta_beg, s);
+    fmeta = upload(L.fmeta, s);
+    fmeta_base = upload(L.fmeta_base, s);
+    tps_beg = upload(L.tps_beg, s);
+    tps = upload(L.tps, s);
     if (L.chained) {
+      imeta_beg = upload(L.imeta_beg, s);
+      imeta = upload(L.imeta, s);
+      imeta_base = upload(L.imeta_base, s);
       it_r = upload(L.it_r, s);
       it_c = upload(L.it_c, s);
       it_h = upload(L.it_h, s);
@@ -403,6 +416,23 @@ struct RankData {
     const size_t esz = data.kind == kAmplitudeF32 ? 4 : 8;
     DevMem neg(sizeof(unsigned long long));
     PDD_CUDA(cudaMemsetAsync(neg.get(), 0, neg.bytes(), s));
+    if (data.kind == kPtyaFramesF64) {  // frames.ptya streamed from disk (ptya.hpp)
+      std::vector<int32_t> g2l(static_cast<size_t>(plan.g.J()), -1);
+      for (int64_t f = 0; f < L.nfr; ++f) g2l[L.fr_global[f]] = static_cast<int32_t>(f);
+      DevMem dg2l = upload(g2l, s);
+      DevMem stage[2];
+      int64_t k = 0;
+      ptya_stream_frames(static_cast<const char*>(data.ptr), plan.g.J(), S, s,
+                         [&](int64_t first, int64_t count, const double* host) {
+                           DevMem& dst = stage[k++ & 1];
+                           const size_t bytes = sizeof(double) * static_cast<size_t>(count * per);
+                           if (dst.bytes() < bytes) dst.alloc(bytes, s);
+                           PDD_CUDA(cudaMemcpyAsync(dst.get(), host, bytes, cudaMemcpyHostToDevice, s));
+                           PDD_CUDA(launch_scatter_amp<T>(dst.as<double>(), first, count, per,
+                                                          dg2l.as<int32_t>(), amp.as<T>(),
+                                                          neg.as<unsigned long long>(), s));
+                         });
+    } else {
     const cudaMemcpyKind kind = data.device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const char* src = static_cast<const char*>(data.ptr);
     // Pageable host input: page-lock it for the duration of the upload (DMA at
@@ -436,6 +466,7 @@ struct RankData {
       }
     }
     pin_src.done();
+    }
     unsigned long long nneg = 0;
     PDD_CUDA(cudaMemcpyAsync(&nneg, neg.get(), sizeof(nneg), cudaMemcpyDeviceToHost, s));
     PDD_CUDA(cudaStreamSynchronize(s));
@@ -510,6 +541,9 @@ struct RankData {
   }
   void set_pieces(GatherArgs<T>& g) const {
     if (!L.chained) return;
+    g.mbeg = imeta_beg.as<int32_t>();
+    g.meta = imeta.as<int4>();
+    g.mbase = imeta_base.as<int64_t>();
     g.tile_items = tile_items.as<int32_t>();
     g.tile_item_beg = tile_item_beg.as<int32_t>();
     g.it_r = it_r.as<int32_t>();
@@ -535,6 +569,11 @@ struct RankData {
     g.sub_w = sub_w.as<int32_t>();
     g.sub_pbeg = sub_pbeg.as<int32_t>();
     g.ps = psides.as<PairSide>();
+    g.mbeg = fmeta_beg.as<int32_t>();  // covering frames (set_pieces switches to the pieces)
+    g.meta = fmeta.as<int4>();
+    g.mbase = fmeta_base.as<int64_t>();
+    g.tps_beg = tps_beg.as<int32_t>();
+    g.tps = tps.as<int32_t>();
     return g;
   }
 
@@ -556,9 +595,32 @@ struct RankData {
     if (comm) comm->allreduce_sum_f64(diff_sub(), 2 * D, s);
   }
 
+  ~RankData() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
+
+  // The overlap consensus of iteration n+1 needs only u^n and Lambda^n, so
+  // it runs as a branch forked off the iteration's start, concurrent with the
+  // frame pass (K1), and joins before the update gather that consumes v.
+  // Its skip flag is the gate's snapshot of earlier iterations' stops (skipC):
+  // a stop decided inside this iteration only discards what the branch wrote.
+  void fork_consensus(const cx<T>* u, const cx<T>* lam, cx<T>* sbuf, cx<T>* v) {
+    if (!ev_fork) {
+      PDD_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      PDD_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    }
+    PDD_CUDA(cudaEventRecord(ev_fork, st()));
+    PDD_CUDA(cudaStreamWaitEvent(side.get(), ev_fork, 0));
+    consensus(u, lam, sbuf, v, skipC(), side.get());
+    PDD_CUDA(cudaEventRecord(ev_join, side.get()));
+  }
+  void join_consensus() { PDD_CUDA(cudaStreamWaitEvent(st(), ev_join, 0)); }
+
   // v = (s_1 + s_2)/2 with s_side = u_side + Lambda_side exchanged across ranks.
-  void consensus(const cx<T>* u, const cx<T>* lam, cx<T>* sbuf, cx<T>* v, const int* skip) {
-    cudaStream_t s = st();
+  void consensus(const cx<T>* u, const cx<T>* lam, cx<T>* sbuf, cx<T>* v, const int* skip,
+                 cudaStream_t s = nullptr) {
+    if (!s) s = st();
     const int np = static_cast<int>(L.lpairs.size());
     PDD_CUDA(launch_pack<T>(pgeom.as<PairGeom>(), np, L.max_pair_pix, u, lam, sbuf, skip, s));
     if (comm && !L.exch.empty()) {

@@ -21,16 +21,15 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // Page-locked download staging (common.cuh HostStage), reserved ahead of use.
 void host_stage_reserve();
 
-// Library-private stream-ordered memory pool per device.  Freed blocks stay
-// mapped while any solver lives on the device (a solver built after another
-// was destroyed reuses its multi-GB buffers instead of paying cudaMalloc's
-// page mapping again: 3-150 ms per solve on c4); when the last one is
-// destroyed the pool is trimmed back to the OS (pdd_release_cached_memory
-// trims on demand).  The device's default pool and every other allocator in
-// the process are left alone.
+// Library-private stream-ordered memory pool per device (device.cpp): freed
+// blocks stay mapped for the next solver (repeated solves skip cudaMalloc's
+// page mapping); pdd_release_cached_memory() returns them, as does the
+// destruction of the last solver on a device with PDD_POOL_TRIM_ON_IDLE=1.
+// The device's default pool and every other allocator in the process are
+// left alone.
 cudaMemPool_t device_pool(int dev);
 void pool_retain(int dev);
-void pool_release(int dev);   // last user on dev: synchronise, trim to 0
+void pool_release(int dev);   // last user on dev: trim if PDD_POOL_TRIM_ON_IDLE=1
 void release_cached_memory();  // all devices
 
 // The stream on which DevMem allocations of this thread are ordered (set by

@@ -29,9 +29,11 @@ struct BlindConfig {  // blind.hpp:7-22
   void validate(int64_t s, const double* mask) const;
 };
 
-enum DataKind { kIntensityF64 = 0, kAmplitudeF32 = 1, kAmplitudeF64 = 2 };
+enum DataKind { kIntensityF64 = 0, kAmplitudeF32 = 1, kAmplitudeF64 = 2, kPtyaFramesF64 = 3 };
 
-// Frames in global scan order, [J][s][s]; host or device memory.
+// Frames in global scan order, [J][s][s]; host or device memory -- or, for
+// kPtyaFramesF64, ptr is a NUL-terminated path of a frames.ptya file
+// (float64 intensities) streamed from disk (ptya.hpp).
 struct DataSpec {
   const void* ptr = nullptr;
   int kind = kIntensityF64;

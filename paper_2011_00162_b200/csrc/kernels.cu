@@ -295,8 +295,9 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
   const int sub = td.x, tr0 = td.y, tc0 = td.z;
   // covering partial images: back-projection pieces, or frames
   const bool items = (MODE == kGatherNonblind || MODE == kGatherAdjoint) && a.tile_items != nullptr;
-  const int fb = items ? a.tile_item_beg[blockIdx.x] : td.w;
-  const int fe = items ? a.tile_item_beg[blockIdx.x + 1] : a.tiles[blockIdx.x + 1].w;
+  const bool flat = a.mbeg != nullptr;  // flattened per-tile lists (one dependent load level)
+  const int fb = flat ? a.mbeg[blockIdx.x] : items ? a.tile_item_beg[blockIdx.x] : td.w;
+  const int fe = flat ? a.mbeg[blockIdx.x + 1] : items ? a.tile_item_beg[blockIdx.x + 1] : a.tiles[blockIdx.x + 1].w;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int H = a.sub_h[sub], W = a.sub_w[sub];
   const int c = tc0 + VEC * tx;  // first of this lane's VEC columns
@@ -325,7 +326,14 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
     const int nk = min(kMeta, nf - kb);
     if (kb > 0) __syncthreads();
     for (int k = threadIdx.x; k < nk; k += blockDim.x) {
-      if (items) {
+      if (flat) {
+        const int4 m = a.meta[fb + kb + k];
+        s_r0[k] = m.x;
+        s_c0[k] = m.y;
+        s_h[k] = m.z;
+        s_fr[k] = m.w;
+        s_base[k] = a.mbase[fb + kb + k];
+      } else if (items) {
         const int it = a.tile_items[fb + kb + k];
         s_fr[k] = -1;
         s_r0[k] = a.it_r[it];
@@ -430,10 +438,19 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
   constexpr bool update = MODE == kGatherNonblind || MODE == kGatherBlind;
   const cx<T>* u_in = a.u_in ? a.u_in : a.u;
   const cx<T>* lam_in = a.lam_in ? a.lam_in : a.lam;
+  // pair sides meeting this tile: the flattened per-tile list (usually empty)
+  // or all of the subdomain's
   int pb = 0, pe = 0;
+  const int32_t* plist = nullptr;
   if constexpr (update) {
-    pb = a.sub_pbeg[sub];
-    pe = a.sub_pbeg[sub + 1];
+    if (a.tps_beg) {
+      pb = a.tps_beg[blockIdx.x];
+      pe = a.tps_beg[blockIdx.x + 1];
+      plist = a.tps;
+    } else {
+      pb = a.sub_pbeg[sub];
+      pe = a.sub_pbeg[sub + 1];
+    }
   }
 #pragma unroll
   for (int i = 0; i < NROW; ++i)
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
       } else {
         cx<T> num = acc[i][v] * a.eta;
         for (int q = pb; q < pe; ++q) {
-          const PairSide p = a.ps[q];
+          const PairSide p = a.ps[plist ? plist[q] : q];
           if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
           const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
           num += (a.v[p.v_off + o] - lam_in[p.lam_off + o]) * a.r;
@@ -466,7 +483,7 @@ __global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGath
           un = rp < T(0) ? cx<T>{T(1), T(0)} : cx<T>{nn.x / dd, nn.y / dd};
         }
         for (int q = pb; q < pe; ++q) {
-          const PairSide p = a.ps[q];
+          const PairSide p = a.ps[plist ? plist[q] : q];
           if (r < p.r0 || r >= p.r1 || cv < p.c0 || cv >= p.c1) continue;
           const int64_t o = static_cast<int64_t>(r - p.r0) * (p.c1 - p.c0) + (cv - p.c0);
           a.lam[p.lam_off + o] = lam_in[p.lam_off + o] + (un - a.v[p.v_off + o]);
@@ -782,6 +799,40 @@ cudaError_t launch_convert_amp(const void* src, int kind, T* amp, int64_t n, uns
   return cudaGetLastError();
 }
 
+// float64 intensities of global frames [g0, g0+count) -> T amplitudes at
+// their local positions (glob2loc: -1 = owned by another rank).
+template <typename T>
+__global__ void scatter_amp_kernel(const double* src, int64_t g0, int64_t count, int64_t per, const int32_t* glob2loc,
+                                   T* amp, unsigned long long* neg) {
+  unsigned long long bad = 0;
+  const int64_t n = count * per;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t f = i / per;
+    const int32_t loc = glob2loc[g0 + f];
+    if (loc < 0) continue;
+    double v = src[i];
+    if (v < 0.0) {
+      ++bad;
+      v = 0.0;
+    }
+    amp[static_cast<int64_t>(loc) * per + (i - f * per)] = static_cast<T>(sqrt(v));
+  }
+  if (bad && neg) atomicAdd(neg, bad);
+}
+template <typename T>
+cudaError_t launch_scatter_amp(const double* src, int64_t g0, int64_t count, int64_t per, const int32_t* glob2loc,
+                               T* amp, unsigned long long* neg, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((count * per + 255) / 256, 148 * 16));
+  scatter_amp_kernel<T><<<grid, 256, 0, st>>>(src, g0, count, per, glob2loc, amp, neg);
+  return cudaGetLastError();
+}
+template cudaError_t launch_scatter_amp<float>(const double*, int64_t, int64_t, int64_t, const int32_t*, float*,
+                                               unsigned long long*, cudaStream_t);
+template cudaError_t launch_scatter_amp<double>(const double*, int64_t, int64_t, int64_t, const int32_t*, double*,
+                                                unsigned long long*, cudaStream_t);
+
 template <typename T>
 __global__ void denom_sub_kernel(const double* dens, const uint8_t* pin, const PairSide* ps, int nps, int H, int W,
                                  T eta, T r, T* denom, unsigned long long* bad, int blind) {
@@ -822,6 +873,7 @@ cudaError_t launch_rpen_sub(const uint8_t* pin, const PairSide* ps, int nps, int
 __global__ void gate_kernel(RunCtl* c) {
   c->skipA = !(c->stop == 0 || (c->stop == c->iter && !c->done));
   c->skipB = c->stop != 0;
+  c->skipC = c->stop != 0;
 }
 __global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, double* rec) {
   if (c->skipA) return;

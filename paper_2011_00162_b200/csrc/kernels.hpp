@@ -47,6 +47,16 @@ struct GatherArgs {
   const int32_t* it_c = nullptr;
   const int32_t* it_h = nullptr;
   const int64_t* it_base = nullptr;
+  // Flattened per-tile lists (layout.cpp, preferred when set): covering
+  // partial images of tile t are entries [mbeg[t], mbeg[t+1]) of meta
+  // {r0, c0, h, frame} and mbase (element offset) -- one dependent load level
+  // fewer than the tile_items -> it_* chain; the pair sides whose overlap
+  // rectangle meets tile t are ps[tps[tps_beg[t] ..]] (usually none).
+  const int32_t* mbeg = nullptr;
+  const int4* meta = nullptr;
+  const int64_t* mbase = nullptr;
+  const int32_t* tps_beg = nullptr;
+  const int32_t* tps = nullptr;
   int S = 0;
   const cx<T>* bp = nullptr;            // [nframes][S][S]
   const cx<T>* probe = nullptr;         // density: P; blind: W copies [nsub][S][S]
@@ -137,6 +147,9 @@ cudaError_t launch_frame_sums(const T* amp, int64_t nfr, int64_t per, double* ou
 // amp[i] = sqrt(src) (kind 0: f64 intensity) or src (kind 1: f32 amplitude, kind 2: f64 amplitude);
 // negative inputs are counted into *neg (FrameStack::validate, scan.cpp:46-56).
 template <typename T>
+cudaError_t launch_scatter_amp(const double* src, int64_t g0, int64_t count, int64_t per, const int32_t* glob2loc,
+                               T* amp, unsigned long long* neg, cudaStream_t st);
+template <typename T>
 cudaError_t launch_convert_amp(const void* src, int kind, T* amp, int64_t n, unsigned long long* neg,
                                cudaStream_t st);
 
@@ -161,7 +174,7 @@ struct RunCtl {
   int skipA;     // frame pass disabled
   int skipB;     // update pass disabled
   int rec_cap;   // records ring capacity (iterations)
-  int pad;
+  int skipC;     // stop from earlier iterations only (set by the gate): the forked consensus branch
   double tol_rf, tol_re, l1;
 };
 cudaError_t launch_gate(RunCtl* c, cudaStream_t st);

@@ -224,7 +224,43 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int
     }
     L.sub_pbeg.push_back(static_cast<int32_t>(L.psides.size()));
   }
+  L.flatten_gather_lists();
   return L;
+}
+
+void Layout::flatten_gather_lists() {
+  const int64_t SS = static_cast<int64_t>(S) * S;
+  fmeta_beg.assign(1, 0);
+  imeta_beg.assign(1, 0);
+  tps_beg.assign(1, 0);
+  fmeta.clear();
+  imeta.clear();
+  fmeta_base.clear();
+  imeta_base.clear();
+  tps.clear();
+  for (int t = 0; t < ntiles(); ++t) {
+    for (int k = tiles[t].w; k < tiles[t + 1].w; ++k) {
+      const int f = tile_frames[k];
+      fmeta.push_back(int4{fr_r[f], fr_c[f], S, f});
+      fmeta_base.push_back(static_cast<int64_t>(f) * SS);
+    }
+    fmeta_beg.push_back(static_cast<int32_t>(fmeta.size()));
+    if (chained) {
+      for (int k = tile_item_beg[t]; k < tile_item_beg[t + 1]; ++k) {
+        const int it = tile_items[k];
+        imeta.push_back(int4{it_r[it], it_c[it], it_h[it], -1});
+        imeta_base.push_back(it_base[it]);
+      }
+      imeta_beg.push_back(static_cast<int32_t>(imeta.size()));
+    }
+    // pair sides of the tile's subdomain whose overlap rectangle meets the tile
+    const int ld = tiles[t].x, r0 = tiles[t].y, c0 = tiles[t].z;
+    for (int q = sub_pbeg[ld]; q < sub_pbeg[ld + 1]; ++q) {
+      const PairSide& p = psides[q];
+      if (p.r0 < r0 + tile_h && r0 < p.r1 && p.c0 < c0 + tile_w && c0 < p.c1) tps.push_back(q);
+    }
+    tps_beg.push_back(static_cast<int32_t>(tps.size()));
+  }
 }
 
 void Layout::schedule(int G) {

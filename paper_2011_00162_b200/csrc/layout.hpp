@@ -81,6 +81,15 @@ struct Layout {
   std::vector<int64_t> cta_ofs;
   void schedule(int G);
 
+  // Flattened gather lists (GatherArgs::mbeg/meta/mbase): per tile, its
+  // covering frames (fmeta) and, chained, its covering pieces (imeta);
+  // meta = {r0, c0, h, frame or -1}.  tps: per tile, the PairSide indices
+  // whose overlap rectangle meets it.
+  std::vector<int32_t> fmeta_beg, imeta_beg, tps_beg, tps;
+  std::vector<int4> fmeta, imeta;
+  std::vector<int64_t> fmeta_base, imeta_base;
+  void flatten_gather_lists();
+
   std::vector<int> lpairs;          // global pair index per local pair
   std::vector<PairGeom> pgeom;      // per local pair
   std::vector<int32_t> sub_pbeg;    // [nls+1] CSR into psides

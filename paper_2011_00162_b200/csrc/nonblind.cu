@@ -6,8 +6,9 @@
 //        -> segsum/[all-reduce] -> rf_finalize (records RF of the previous
 //           iterate and applies the R-factor stop rule with Gamma ping-pong
 //           so a stop rolls back for free)
-//        -> pack s = u + Lambda -> [NCCL send/recv per cut pair] -> v-step
-//        -> gather (adjoint overlap-add + u-update + Lambda-update + RE)
+//        -> [join] gather (adjoint overlap-add + u-update + Lambda-update + RE)
+//   branch forked at the gate, concurrent with the frame pass:
+//           pack s = u + Lambda -> [NCCL send/recv per cut pair] -> v-step
 //        -> segsum/[all-reduce] -> re_finalize (RE stop rule, max_iters)
 // Two iterations (Gamma parities) per graph.  The R-factor of iterate n is
 // produced by the frame pass of iteration n+1 (its forward transform is the
@@ -165,6 +166,9 @@ class Nonblind final : public NonblindGpu {
   void enqueue_iteration(int parity, bool store_z, cudaEvent_t* ev = nullptr) {
     cudaStream_t s = R.st();
     PDD_CUDA(launch_gate(R.ctlp(), s));
+    // v^{n+1} from u^n, Lambda^n (solver.cpp:141-151) into the outgoing
+    // parity, on a branch concurrent with the frame pass
+    R.fork_consensus(U(parity), LAM(parity), s_.as<cx<T>>(), V(1 - parity));
     if (ev) PDD_CUDA(cudaEventRecord(ev[0], s));
     FrameArgs<T> a = R.frame_args();
     a.probe = probe_.as<cx<T>>();
@@ -183,8 +187,7 @@ class Nonblind final : public NonblindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
     R.reduce_rf(true);
     PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
-    // v^{n+1} from u^n, Lambda^n (solver.cpp:141-151) into the outgoing parity
-    R.consensus(U(parity), LAM(parity), s_.as<cx<T>>(), V(1 - parity), R.skipB());
+    R.join_consensus();
     GatherArgs<T> g = R.gather_args(kGatherNonblind);
     R.set_pieces(g);
     g.bp = bp_.as<cx<T>>();

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
 from dataclasses import dataclass, field
@@ -31,8 +32,8 @@ from typing import Callable, List, Optional, Sequence
 import numpy as np
 
 from . import _lib as L
-from ._lib import (CudaError, DivergenceError, InvalidArgument, OutOfRange, PtychoRuntimeError, c128, check, f64,
-                   i64, ptr)
+from ._lib import (CudaError, DivergenceError, FormatError, InvalidArgument, OutOfRange, PtychoRuntimeError, c128,
+                   check, f64, i64, ptr)
 
 DEFAULT_DTYPE = "f64"
 
@@ -560,6 +561,16 @@ class _DataArg:
         if (frames is None) == (amplitudes is None):
             raise InvalidArgument("give exactly one of frames (intensities) or amplitudes")
         a = frames if frames is not None else amplitudes
+        self.path = None
+        if frames is not None and isinstance(frames, (str, os.PathLike)):
+            # a frames.ptya file: streamed from disk to the device by the library
+            from . import ptya
+
+            self.path = os.fsencode(frames)
+            self.arr, self.kind, self.on_device = C.c_char_p(self.path), L.DATA_PTYA_FRAMES_F64, False
+            self.shape = ptya.header(frames, ptya.F64)[0]
+            self._file = frames
+            return
         self.on_device = bool(hasattr(a, "is_cuda") and a.is_cuda)
         if self.on_device:
             import torch
@@ -589,6 +600,10 @@ class _DataArg:
             raise InvalidArgument("FrameStack: frame count != scan position count or frame shape mismatch")
 
     def host_sqrt(self):
+        if self.path is not None:
+            from . import ptya
+
+            return np.sqrt(ptya.read_frames(self._file))
         if self.on_device:
             a = self.arr.double().cpu().numpy()
         else:

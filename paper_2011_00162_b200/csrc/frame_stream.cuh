@@ -77,6 +77,17 @@ struct ProbeTmem {
 #define PDD_COLSPLIT 2  // column groups: independent warp sets exchanging through named barriers
 #endif
 
+#ifndef PDD_TWC_CONST
+#define PDD_TWC_CONST 0  // column-phase twiddles (warp-uniform index) from constant memory
+#endif
+#ifndef PDD_TWR_CONST
+#define PDD_TWR_CONST 0  // row-phase inter-stage twiddles from constant memory (8 addresses per warp)
+#endif
+#if PDD_TWC_CONST || PDD_TWR_CONST
+__constant__ float2 c_twc[128];  // [gc][k] = W_128^(gc k), filled by launch_stream
+__constant__ float2 c_twr[128];  // [k][g] = W_128^(g k)
+#endif
+
 // Two twiddles W[k], W[k+1] (k even) by one 16-byte shared-memory load.
 __device__ __forceinline__ void tw_pair(const cx<float>* p, cx<float>& a, cx<float>& b) {
   const float4 v = *reinterpret_cast<const float4*>(p);
@@ -121,6 +132,24 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // column phase split into NSPLIT independent warp sets (S = 128 float sweep)
   constexpr int NSPLIT = (std::is_same_v<T, float> && S == 128 && CG % PDD_COLSPLIT == 0 &&
                           (NT / 32) % PDD_COLSPLIT == 0) ? PDD_COLSPLIT : 1;
+  constexpr bool CTW = PDD_TWC_CONST && std::is_same_v<T, float> && S == 128 && RC == 16;
+  constexpr bool RTW = PDD_TWR_CONST && std::is_same_v<T, float> && S == 128 && GR == 8;
+  auto ctw = [](int i) {
+#if PDD_TWC_CONST
+    const float2 v = c_twc[i];
+    return cx<T>{T(v.x), T(v.y)};
+#else
+    return cx<T>{T(0), T(0)};
+#endif
+  };
+  auto rtw = [](int i) {
+#if PDD_TWR_CONST
+    const float2 v = c_twr[i];
+    return cx<T>{T(v.x), T(v.y)};
+#else
+    return cx<T>{T(0), T(0)};
+#endif
+  };
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
   cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
   cx<T>* twc = twr + S;  // column-phase twiddles, [gc][k] = W_S^(gc k): immediate offsets in k
@@ -339,6 +368,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k = 0; k < RR; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
+        else if constexpr (RTW) t0 = rtw(k * GR + g), t1 = rtw((k + 1) * GR + g);
         else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
         buf[y * P + k * GR + ((g + k) & (GR - 1))] = (k == 0) ? v[k] : v[k] * t0;
         buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))] = v[k + 1] * t1;
@@ -408,6 +438,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k = 0; k < RC; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
+        else if constexpr (CTW) t0 = ctw(gc * RC + k), t1 = ctw(gc * RC + k + 1);
         else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
         buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * t0;
         buf[((k + 1) * GC + gc) * P + x] = w[k + 1] * t1;
@@ -481,6 +512,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k = 0; k < RC; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
+        else if constexpr (CTW) t0 = ctw(gc * RC + k), t1 = ctw(gc * RC + k + 1);
         else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
         const cx<T> v0 = buf[(k * GC + gc) * P + x], v1 = buf[((k + 1) * GC + gc) * P + x];
         w[k] = (k == 0) ? v0 : mul_conj(v0, t0);
@@ -536,6 +568,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k = 0; k < RR; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
+        else if constexpr (RTW) t0 = rtw(k * GR + g), t1 = rtw((k + 1) * GR + g);
         else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
         const cx<T> b0 = buf[y * P + k * GR + ((g + k) & (GR - 1))];
         const cx<T> b1 = buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))];

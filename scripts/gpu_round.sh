@@ -4,7 +4,7 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 TAG=${TAG:-r1}
-timeout 900 python -m pytest tests/ -q -m gpu > gpurun_out/tests_$TAG.log 2>&1
+timeout ${TEST_TIMEOUT:-2400} python -m pytest tests/ -q -m gpu > gpurun_out/tests_$TAG.log 2>&1
 tail -n 1 gpurun_out/tests_$TAG.log
 bash scripts/gpu_bench.sh
 if [ "${NCU:-1}" = 1 ]; then

@@ -80,6 +80,30 @@ struct ProbeTmem {
 #ifndef PDD_TWC_CONST
 #define PDD_TWC_CONST 0  // column-phase twiddles (warp-uniform index) from constant memory
 #endif
+#ifdef PDD_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[4];  // summed over CTAs; printed by launch_stream
+#endif
+#ifndef PDD_LDORD
+#define PDD_LDORD 0  // shared-memory loads issued in butterfly-partner order
+#endif
+#ifndef PDD_SKEW
+#define PDD_SKEW 2000  // cycles by which column warp set k starts after set k-1 (see "Staggered warps")
+#endif
+#ifndef PDD_AMP16
+#define PDD_AMP16 0  // amplitude tile staged by the warp set in 16-byte cp.async chunks (shared by its threads)
+#endif
+#ifndef PDD_CHAINC
+#define PDD_CHAINC 0  // column sets chained: set 1 starts when set 0 reaches point 1|2|3 of its first group
+#endif
+#ifndef PDD_CHAINR
+#define PDD_CHAINR 1  // row phases chained by warp rank on the scheduler: rank k starts when rank k-1 passed point 1|2|3
+#endif
+#ifndef PDD_SKEWR
+#define PDD_SKEWR 0  // experiment: row-phase stagger (cycles) per warp rank on its scheduler
+#endif
+#ifndef PDD_SKEWR_MODE
+#define PDD_SKEWR_MODE 0  // 0: delay = (warp / 4) * SKEWR; 1: warps 8-15 delayed by SKEWR
+#endif
 #ifndef PDD_TWR_CONST
 #define PDD_TWR_CONST 0  // row-phase inter-stage twiddles from constant memory (8 addresses per warp)
 #endif
@@ -96,6 +120,9 @@ __device__ __forceinline__ void tw_pair(const cx<float>* p, cx<float>& a, cx<flo
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 #ifndef PDD_STAGE64
@@ -136,16 +163,18 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   constexpr bool RTW = PDD_TWR_CONST && std::is_same_v<T, float> && S == 128 && GR == 8;
   auto ctw = [](int i) {
 #if PDD_TWC_CONST
-    const float2 v = c_twc[i];
-    return cx<T>{T(v.x), T(v.y)};
+    float vx, vy;  // volatile: no common-subexpression reuse across the phase (register pressure)
+    asm volatile("ld.const.v2.f32 {%0, %1}, [%2];" : "=f"(vx), "=f"(vy) : "l"(c_twc + i));
+    return cx<T>{T(vx), T(vy)};
 #else
     return cx<T>{T(0), T(0)};
 #endif
   };
   auto rtw = [](int i) {
 #if PDD_TWR_CONST
-    const float2 v = c_twr[i];
-    return cx<T>{T(v.x), T(v.y)};
+    float vx, vy;  // volatile: no common-subexpression reuse across the phase (register pressure)
+    asm volatile("ld.const.v2.f32 {%0, %1}, [%2];" : "=f"(vx), "=f"(vy) : "l"(c_twr + i));
+    return cx<T>{T(vx), T(vy)};
 #else
     return cx<T>{T(0), T(0)};
 #endif
@@ -275,9 +304,30 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   cx<T> pg[RC];
   constexpr bool STAGE = amp_tile_staged<T, SH, FWD>();
   T pa[STAGE ? 1 : RC];
+  // COOP: a warp set stages its [S ky][SETC kx] amplitude sub-tile of the next
+  // column group together, 16 bytes per cp.async (4 instead of 16 copies per
+  // thread, whole 128-byte rows per quarter warp); issued after the group's
+  // inverse exchange barrier (every thread of the set is then past its prox)
+  // and completed before the next group's forward exchange barrier.
+  constexpr bool COOP = PDD_AMP16 && STAGE && !FWD && !ADJ && NSPLIT == 2 && SETC == 32 && RC * NT == 2 * S * SETC;
   auto pa_at = [&](int e) {
-    if constexpr (STAGE) return ampst[e * NT + t];
+    if constexpr (COOP) return ampst[(t / SETT) * (S * SETC) + (gc + GC * (e / GC) + RC * (e % GC)) * SETC + (t & 31)];
+    else if constexpr (STAGE) return ampst[e * NT + t];
     else return pa[e];
+  };
+  auto prefetch_amp = [&](int ff, int grp) {  // COOP only
+    if constexpr (COOP) {
+      if (ff < 0) return;
+      const int ts = t % SETT, set = t / SETT;
+      const T* asrc = a.amp + static_cast<int64_t>(ff) * S * S + grp * CG + set * SETC;
+      T* dst = ampst + set * (S * SETC);
+#pragma unroll
+      for (int j = 0; j < (S * SETC / 4) / SETT; ++j) {
+        const int c = ts + SETT * j, ky = c >> 3, part = c & 7;
+        cp_async16(dst + ky * SETC + part * 4, asrc + ky * S + part * 4);
+      }
+      cp_async_commit();
+    }
   };
   auto prefetch = [&](int ff, int grp) {
     if (ff < 0) return;
@@ -298,12 +348,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         const int oy = GC * q + RC * k1;
         if constexpr (!FWD) pg[q * GC + k1] = gsrc[oy * S];
         if constexpr (ADJ) continue;
+        if constexpr (COOP) continue;
         if (!FWD || a.rf_part) {
           if constexpr (STAGE) cp_async4(ampst + (q * GC + k1) * NT + t, asrc + oy * S);
           else pa[q * GC + k1] = asrc[oy * S];
         }
       }
-    if constexpr (STAGE) cp_async_commit();
+    if constexpr (STAGE && !COOP) cp_async_commit();
   };
 #ifdef PDD_CANARY  // debug builds: detect shared-memory writes past the working set
   uint32_t* canary = reinterpret_cast<uint32_t*>(smem_raw + stream_smem_bytes_base<T, SH>());
@@ -325,6 +376,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   {
     const int f0 = frame_at(i);
     prefetch(f0, 0);
+    prefetch_amp(f0, 0);
     if (tma_rows && f0 >= 0)
 #pragma unroll 1
       for (int rb = 0; rb < NRB; ++rb) issue_rows(f0, rb);
@@ -352,8 +404,16 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       cx<T> v[RR], pv[RR];
       if (tma_rows) {
         mbar_wait(s_rowbar + rb * NW + warp, row_phase);
+#if PDD_LDORD
+#pragma unroll
+        for (int m = 0; m < RR / 2; ++m) {
+          v[m] = buf[y * P + g + GR * m];
+          v[m + RR / 2] = buf[y * P + g + GR * (m + RR / 2)];
+        }
+#else
 #pragma unroll
         for (int m = 0; m < RR; ++m) v[m] = buf[y * P + g + GR * m];
+#endif
         __syncwarp();  // all lanes hold their row elements before the row is overwritten
       } else {
         const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
@@ -409,7 +469,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     __syncthreads();
     if constexpr (ACC) tmem_fence_after_sync();
     if constexpr (FUSE) {
-      if (pend_f >= 0 && a.rf_part && t == 0) {
+      // summed by the first thread of the LAST warp set, which starts its
+      // columns late anyway (staggered sets below)
+      if (pend_f >= 0 && a.rf_part && t == NT - NT / NSPLIT) {
         double s = 0.0;
         for (int w = 0; w < NT / 32; ++w) s += red[w];
         a.rf_part[pend_f] = s;
@@ -417,6 +479,22 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
     PDD_TICK(0);
 
+#if PDD_SKEW
+    // Staggered warps: after a CTA barrier all 16 warps run the same
+    // shared-memory burst / FMA burst sequence in lockstep, so the two pipes
+    // take turns instead of overlapping.  Starting warp set k late by
+    // k * PDD_SKEW cycles keeps one set in its exchange while the other
+    // computes (measured on config 4: K1 7.63 -> 7.30 ms at 2000 cycles).
+    if (NSPLIT >= 2 && t >= SETT) {
+      const long long t0 = clock64();
+      const long long d = static_cast<long long>(PDD_SKEW) * (t / SETT);
+      while (clock64() - t0 < d) {
+      }
+    }
+#endif
+    if constexpr (PDD_CHAINC != 0 && NSPLIT == 2) {
+      if (t >= SETT) named_bar(8, NT);  // set 1 starts once set 0 is one exchange ahead
+    }
     // ---------------- column groups: forward, prox, inverse
     T rf_acc = T(0);  // <= 2*RC terms per thread: float is ample; the tree below is double
 #pragma unroll 1
@@ -431,8 +509,16 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         if (grp + 1 < NG) prefetch(f, grp + 1);
         else prefetch(frame_at(next_of(i)), 0);
       } else {
+#if PDD_LDORD
+#pragma unroll
+      for (int m = 0; m < RC / 2; ++m) {  // butterfly partners (m, m + RC/2) loaded back to back
+        w[m] = buf[(gc + GC * m) * P + x];
+        w[m + RC / 2] = buf[(gc + GC * (m + RC / 2)) * P + x];
+      }
+#else
 #pragma unroll
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
+#endif
       dft<RC, false>(w);
 #pragma unroll
       for (int k = 0; k < RC; k += 2) {
@@ -443,7 +529,14 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * t0;
         buf[((k + 1) * GC + gc) * P + x] = w[k + 1] * t1;
       }
+      if constexpr (PDD_CHAINC == 1 && NSPLIT == 2) {
+        if (grp == 0 && t < SETT) named_arrive(8, NT);
+      }
+      if constexpr (COOP) cp_async_wait_all();  // this thread's chunks of the set's amplitude tile
       col_sync();
+      if constexpr (PDD_CHAINC == 2 && NSPLIT == 2) {
+        if (grp == 0 && t < SETT) named_arrive(8, NT);
+      }
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
         const int k2 = gc + GC * q;
@@ -451,8 +544,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int gp = 0; gp < GC; ++gp) w[q * GC + gp] = buf[(k2 * GC + gp) * P + x];
         dft<GC, false>(w + q * GC);
       }
+      if constexpr (PDD_CHAINC == 3 && NSPLIT == 2) {
+        if (grp == 0 && t < SETT) named_arrive(8, NT);
+      }
       // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
-      if constexpr (STAGE) cp_async_wait_all();  // this thread's staged amplitudes
+      if constexpr (STAGE && !COOP) cp_async_wait_all();  // this thread's staged amplitudes
       T acc = T(0);
       const int64_t fx = fbase + gc * S + x;  // + (ky - gc) * S below, immediates
       if constexpr (FWD) {
@@ -508,6 +604,10 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int gp = 0; gp < GC; ++gp) buf[(k2 * GC + gp) * P + x] = w[q * GC + gp];
       }
       col_sync();
+      if constexpr (COOP) {
+        if (grp + 1 < NG) prefetch_amp(f, grp + 1);
+        else prefetch_amp(frame_at(next_of(i)), 0);
+      }
 #pragma unroll
       for (int k = 0; k < RC; k += 2) {
         cx<T> t0, t1;
@@ -544,6 +644,22 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       __trap();
     }
 #endif
+#if PDD_SKEWR
+    if (!FWD && (warp >> 2) > 0) {  // experiment: stagger the warps of each scheduler in the row phases
+      const long long t0 = clock64();
+      const long long d = static_cast<long long>(PDD_SKEWR) * (PDD_SKEWR_MODE == 0 ? (warp >> 2) : ((warp >> 3) & 1));
+      while (clock64() - t0 < d) {
+      }
+    }
+#endif
+    // Staggered row phases: the four warps of a scheduler (ranks warp / 4)
+    // start one after the other -- rank k once rank k-1 has issued its first
+    // exchange -- so their shared-memory bursts and FFT arithmetic interleave
+    // instead of coinciding (config 4: K1 7.30 -> 6.99 ms with the column stagger).
+    constexpr bool CHR = PDD_CHAINR != 0 && !FWD && NW == 16;
+    if constexpr (CHR) {
+      if ((warp >> 2) > 0) named_bar(8 + (warp >> 2), 256);  // rank k waits for rank k-1
+    }
 #pragma unroll 1
     for (int rb = 0; rb < (FWD ? 0 : NRB); ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
@@ -556,12 +672,18 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int k1 = 0; k1 < GR; ++k1) v[q * GR + k1] = buf[y * P + k2 + RR * k1];
         dft<GR, true>(v + q * GR);
       }
+      if constexpr (CHR && PDD_CHAINR == 1) {
+        if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
+      }
       __syncwarp();
 #pragma unroll
       for (int q = 0; q < RR / GR; ++q) {
         const int k2 = g + GR * q;
 #pragma unroll
         for (int gp = 0; gp < GR; ++gp) buf[y * P + k2 * GR + ((gp + k2) & (GR - 1))] = v[q * GR + gp];
+      }
+      if constexpr (CHR && PDD_CHAINR == 2) {
+        if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
       }
       __syncwarp();
 #pragma unroll
@@ -574,6 +696,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         const cx<T> b1 = buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))];
         v[k] = (k == 0) ? b0 : mul_conj(b0, t0);
         v[k + 1] = mul_conj(b1, t1);
+      }
+      if constexpr (CHR && PDD_CHAINR == 3) {
+        if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
       }
       if (tma_rows && fn >= 0) {
         __syncwarp();             // this warp's rows are consumed
@@ -659,8 +784,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
 #endif
 #ifdef PDD_PHASE_TIMING
-  if (a.phase_cycles && t == 0)
-    for (int i = 0; i < 4; ++i) atomicAdd(a.phase_cycles + i, tph[i]);
+  if (t == 0)
+    for (int i = 0; i < 4; ++i) atomicAdd(g_phase_cycles + i, tph[i]);
 #endif
 #undef PDD_TICK
   if constexpr (TMEMP) {

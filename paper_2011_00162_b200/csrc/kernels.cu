@@ -100,6 +100,20 @@ static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
   if (tile_in_global<T, SH>() && !a.scratch) return cudaErrorInvalidValue;
   const int grid = (FWD || ADJ) ? std::min(a.nframes, blocks_per_sm * sms) : a.ncta;
   kern<<<grid, SH::NT, smem, st>>>(a);
+#ifdef PDD_PHASE_TIMING  // diagnostic builds (not capturable): per-phase cycles summed over CTAs
+  {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusNone) {
+      cudaStreamSynchronize(st);
+      unsigned long long h[4] = {0, 0, 0, 0}, z[4] = {0, 0, 0, 0};
+      cudaMemcpyFromSymbol(h, g_phase_cycles, sizeof(h));
+      cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+      fprintf(stderr, "PDD_PHASE S=%d FWD=%d grid=%d frames=%d: barrier+rfsum %.0f  columns %.0f  rows_inv %.0f  rows_fwd_next %.0f (cycles per CTA)\n",
+              SH::S, int(FWD), grid, a.nframes, double(h[0]) / grid, double(h[1]) / grid, double(h[2]) / grid, double(h[3]) / grid);
+    }
+  }
+#endif
   return cudaGetLastError();
 }
 

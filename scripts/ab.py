@@ -25,7 +25,8 @@ def build(pairs):
     B.build()
     os.makedirs(BIN, exist_ok=True)
     objs = [os.path.join(B.BUILD, os.path.basename(s) + ".o") for s in B._sources()]
-    for name, flags in pairs:
+    def one(pair):
+        name, flags = pair
         vobjs = list(objs)
         for u in UNITS:
             src = os.path.join(B.CSRC, u)
@@ -39,7 +40,11 @@ def build(pairs):
             vobjs[objs.index(os.path.join(B.BUILD, u + ".o"))] = obj
         lib = os.path.join(BIN, f"lib_{name}.so")
         subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", lib, *vobjs, "-ldl", "-lpthread"], check=True)
-        print("built", lib)
+        print("built", lib, flush=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        list(ex.map(one, pairs))
 
 
 def run(config, iters, names):
@@ -51,6 +56,8 @@ def run(config, iters, names):
                            env=env, capture_output=True, text=True)
         out = (r.stdout.strip().splitlines() or ["<no output>"])[-1]
         print(f"{n:>16}: {out}" + ("" if r.returncode == 0 else f"  [rc {r.returncode}] {r.stderr[-400:]}"), flush=True)
+        for ln in [x for x in r.stderr.splitlines() if x.startswith("PDD_PHASE")][-3:]:
+            print(" " * 18 + ln, flush=True)
 
 
 if __name__ == "__main__":

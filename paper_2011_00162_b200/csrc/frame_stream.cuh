@@ -77,39 +77,14 @@ struct ProbeTmem {
 #define PDD_COLSPLIT 2  // column groups: independent warp sets exchanging through named barriers
 #endif
 
-#ifndef PDD_TWC_CONST
-#define PDD_TWC_CONST 0  // column-phase twiddles (warp-uniform index) from constant memory
-#endif
 #ifdef PDD_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[4];  // summed over CTAs; printed by launch_stream
-#endif
-#ifndef PDD_LDORD
-#define PDD_LDORD 0  // shared-memory loads issued in butterfly-partner order
 #endif
 #ifndef PDD_SKEW
 #define PDD_SKEW 2000  // cycles by which column warp set k starts after set k-1 (see "Staggered warps")
 #endif
-#ifndef PDD_AMP16
-#define PDD_AMP16 0  // amplitude tile staged by the warp set in 16-byte cp.async chunks (shared by its threads)
-#endif
-#ifndef PDD_CHAINC
-#define PDD_CHAINC 0  // column sets chained: set 1 starts when set 0 reaches point 1|2|3 of its first group
-#endif
 #ifndef PDD_CHAINR
-#define PDD_CHAINR 1  // row phases chained by warp rank on the scheduler: rank k starts when rank k-1 passed point 1|2|3
-#endif
-#ifndef PDD_SKEWR
-#define PDD_SKEWR 0  // experiment: row-phase stagger (cycles) per warp rank on its scheduler
-#endif
-#ifndef PDD_SKEWR_MODE
-#define PDD_SKEWR_MODE 0  // 0: delay = (warp / 4) * SKEWR; 1: warps 8-15 delayed by SKEWR
-#endif
-#ifndef PDD_TWR_CONST
-#define PDD_TWR_CONST 0  // row-phase inter-stage twiddles from constant memory (8 addresses per warp)
-#endif
-#if PDD_TWC_CONST || PDD_TWR_CONST
-__constant__ float2 c_twc[128];  // [gc][k] = W_128^(gc k), filled by launch_stream
-__constant__ float2 c_twr[128];  // [k][g] = W_128^(g k)
+#define PDD_CHAINR 1  // row phases chained by warp rank on the scheduler: rank k starts when rank k-1 issued its first exchange
 #endif
 
 // Two twiddles W[k], W[k+1] (k even) by one 16-byte shared-memory load.
@@ -159,26 +134,6 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // column phase split into NSPLIT independent warp sets (S = 128 float sweep)
   constexpr int NSPLIT = (std::is_same_v<T, float> && S == 128 && CG % PDD_COLSPLIT == 0 &&
                           (NT / 32) % PDD_COLSPLIT == 0) ? PDD_COLSPLIT : 1;
-  constexpr bool CTW = PDD_TWC_CONST && std::is_same_v<T, float> && S == 128 && RC == 16;
-  constexpr bool RTW = PDD_TWR_CONST && std::is_same_v<T, float> && S == 128 && GR == 8;
-  auto ctw = [](int i) {
-#if PDD_TWC_CONST
-    float vx, vy;  // volatile: no common-subexpression reuse across the phase (register pressure)
-    asm volatile("ld.const.v2.f32 {%0, %1}, [%2];" : "=f"(vx), "=f"(vy) : "l"(c_twc + i));
-    return cx<T>{T(vx), T(vy)};
-#else
-    return cx<T>{T(0), T(0)};
-#endif
-  };
-  auto rtw = [](int i) {
-#if PDD_TWR_CONST
-    float vx, vy;  // volatile: no common-subexpression reuse across the phase (register pressure)
-    asm volatile("ld.const.v2.f32 {%0, %1}, [%2];" : "=f"(vx), "=f"(vy) : "l"(c_twr + i));
-    return cx<T>{T(vx), T(vy)};
-#else
-    return cx<T>{T(0), T(0)};
-#endif
-  };
   cx<T>* tw = reinterpret_cast<cx<T>*>(smem_raw);
   cx<T>* twr = tw + S;  // row-phase inter-stage twiddles, [k][g] = W_S^(g k): lane-consecutive reads
   cx<T>* twc = twr + S;  // column-phase twiddles, [gc][k] = W_S^(gc k): immediate offsets in k
@@ -304,30 +259,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   cx<T> pg[RC];
   constexpr bool STAGE = amp_tile_staged<T, SH, FWD>();
   T pa[STAGE ? 1 : RC];
-  // COOP: a warp set stages its [S ky][SETC kx] amplitude sub-tile of the next
-  // column group together, 16 bytes per cp.async (4 instead of 16 copies per
-  // thread, whole 128-byte rows per quarter warp); issued after the group's
-  // inverse exchange barrier (every thread of the set is then past its prox)
-  // and completed before the next group's forward exchange barrier.
-  constexpr bool COOP = PDD_AMP16 && STAGE && !FWD && !ADJ && NSPLIT == 2 && SETC == 32 && RC * NT == 2 * S * SETC;
   auto pa_at = [&](int e) {
-    if constexpr (COOP) return ampst[(t / SETT) * (S * SETC) + (gc + GC * (e / GC) + RC * (e % GC)) * SETC + (t & 31)];
-    else if constexpr (STAGE) return ampst[e * NT + t];
+    if constexpr (STAGE) return ampst[e * NT + t];
     else return pa[e];
-  };
-  auto prefetch_amp = [&](int ff, int grp) {  // COOP only
-    if constexpr (COOP) {
-      if (ff < 0) return;
-      const int ts = t % SETT, set = t / SETT;
-      const T* asrc = a.amp + static_cast<int64_t>(ff) * S * S + grp * CG + set * SETC;
-      T* dst = ampst + set * (S * SETC);
-#pragma unroll
-      for (int j = 0; j < (S * SETC / 4) / SETT; ++j) {
-        const int c = ts + SETT * j, ky = c >> 3, part = c & 7;
-        cp_async16(dst + ky * SETC + part * 4, asrc + ky * S + part * 4);
-      }
-      cp_async_commit();
-    }
   };
   auto prefetch = [&](int ff, int grp) {
     if (ff < 0) return;
@@ -348,13 +282,12 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         const int oy = GC * q + RC * k1;
         if constexpr (!FWD) pg[q * GC + k1] = gsrc[oy * S];
         if constexpr (ADJ) continue;
-        if constexpr (COOP) continue;
         if (!FWD || a.rf_part) {
           if constexpr (STAGE) cp_async4(ampst + (q * GC + k1) * NT + t, asrc + oy * S);
           else pa[q * GC + k1] = asrc[oy * S];
         }
       }
-    if constexpr (STAGE && !COOP) cp_async_commit();
+    if constexpr (STAGE) cp_async_commit();
   };
 #ifdef PDD_CANARY  // debug builds: detect shared-memory writes past the working set
   uint32_t* canary = reinterpret_cast<uint32_t*>(smem_raw + stream_smem_bytes_base<T, SH>());
@@ -376,7 +309,6 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   {
     const int f0 = frame_at(i);
     prefetch(f0, 0);
-    prefetch_amp(f0, 0);
     if (tma_rows && f0 >= 0)
 #pragma unroll 1
       for (int rb = 0; rb < NRB; ++rb) issue_rows(f0, rb);
@@ -404,16 +336,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       cx<T> v[RR], pv[RR];
       if (tma_rows) {
         mbar_wait(s_rowbar + rb * NW + warp, row_phase);
-#if PDD_LDORD
-#pragma unroll
-        for (int m = 0; m < RR / 2; ++m) {
-          v[m] = buf[y * P + g + GR * m];
-          v[m + RR / 2] = buf[y * P + g + GR * (m + RR / 2)];
-        }
-#else
 #pragma unroll
         for (int m = 0; m < RR; ++m) v[m] = buf[y * P + g + GR * m];
-#endif
         __syncwarp();  // all lanes hold their row elements before the row is overwritten
       } else {
         const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
@@ -428,7 +352,6 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       for (int k = 0; k < RR; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
-        else if constexpr (RTW) t0 = rtw(k * GR + g), t1 = rtw((k + 1) * GR + g);
         else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
         buf[y * P + k * GR + ((g + k) & (GR - 1))] = (k == 0) ? v[k] : v[k] * t0;
         buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))] = v[k + 1] * t1;
@@ -492,9 +415,6 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
     }
 #endif
-    if constexpr (PDD_CHAINC != 0 && NSPLIT == 2) {
-      if (t >= SETT) named_bar(8, NT);  // set 1 starts once set 0 is one exchange ahead
-    }
     // ---------------- column groups: forward, prox, inverse
     T rf_acc = T(0);  // <= 2*RC terms per thread: float is ample; the tree below is double
 #pragma unroll 1
@@ -509,34 +429,18 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         if (grp + 1 < NG) prefetch(f, grp + 1);
         else prefetch(frame_at(next_of(i)), 0);
       } else {
-#if PDD_LDORD
-#pragma unroll
-      for (int m = 0; m < RC / 2; ++m) {  // butterfly partners (m, m + RC/2) loaded back to back
-        w[m] = buf[(gc + GC * m) * P + x];
-        w[m + RC / 2] = buf[(gc + GC * (m + RC / 2)) * P + x];
-      }
-#else
 #pragma unroll
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
-#endif
       dft<RC, false>(w);
 #pragma unroll
       for (int k = 0; k < RC; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
-        else if constexpr (CTW) t0 = ctw(gc * RC + k), t1 = ctw(gc * RC + k + 1);
         else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
         buf[(k * GC + gc) * P + x] = (k == 0) ? w[k] : w[k] * t0;
         buf[((k + 1) * GC + gc) * P + x] = w[k + 1] * t1;
       }
-      if constexpr (PDD_CHAINC == 1 && NSPLIT == 2) {
-        if (grp == 0 && t < SETT) named_arrive(8, NT);
-      }
-      if constexpr (COOP) cp_async_wait_all();  // this thread's chunks of the set's amplitude tile
       col_sync();
-      if constexpr (PDD_CHAINC == 2 && NSPLIT == 2) {
-        if (grp == 0 && t < SETT) named_arrive(8, NT);
-      }
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
         const int k2 = gc + GC * q;
@@ -544,11 +448,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int gp = 0; gp < GC; ++gp) w[q * GC + gp] = buf[(k2 * GC + gp) * P + x];
         dft<GC, false>(w + q * GC);
       }
-      if constexpr (PDD_CHAINC == 3 && NSPLIT == 2) {
-        if (grp == 0 && t < SETT) named_arrive(8, NT);
-      }
       // Fourier-domain step: w[q*GC + k1] = X(ky = gc + GC q + RC k1, kx = x)
-      if constexpr (STAGE && !COOP) cp_async_wait_all();  // this thread's staged amplitudes
+      if constexpr (STAGE) cp_async_wait_all();  // this thread's staged amplitudes
       T acc = T(0);
       const int64_t fx = fbase + gc * S + x;  // + (ky - gc) * S below, immediates
       if constexpr (FWD) {
@@ -604,15 +505,10 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int gp = 0; gp < GC; ++gp) buf[(k2 * GC + gp) * P + x] = w[q * GC + gp];
       }
       col_sync();
-      if constexpr (COOP) {
-        if (grp + 1 < NG) prefetch_amp(f, grp + 1);
-        else prefetch_amp(frame_at(next_of(i)), 0);
-      }
 #pragma unroll
       for (int k = 0; k < RC; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twc + gc * RC + k, t0, t1);
-        else if constexpr (CTW) t0 = ctw(gc * RC + k), t1 = ctw(gc * RC + k + 1);
         else t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
         const cx<T> v0 = buf[(k * GC + gc) * P + x], v1 = buf[((k + 1) * GC + gc) * P + x];
         w[k] = (k == 0) ? v0 : mul_conj(v0, t0);
@@ -644,14 +540,6 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       __trap();
     }
 #endif
-#if PDD_SKEWR
-    if (!FWD && (warp >> 2) > 0) {  // experiment: stagger the warps of each scheduler in the row phases
-      const long long t0 = clock64();
-      const long long d = static_cast<long long>(PDD_SKEWR) * (PDD_SKEWR_MODE == 0 ? (warp >> 2) : ((warp >> 3) & 1));
-      while (clock64() - t0 < d) {
-      }
-    }
-#endif
     // Staggered row phases: the four warps of a scheduler (ranks warp / 4)
     // start one after the other -- rank k once rank k-1 has issued its first
     // exchange -- so their shared-memory bursts and FFT arithmetic interleave
@@ -672,7 +560,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int k1 = 0; k1 < GR; ++k1) v[q * GR + k1] = buf[y * P + k2 + RR * k1];
         dft<GR, true>(v + q * GR);
       }
-      if constexpr (CHR && PDD_CHAINR == 1) {
+      if constexpr (CHR) {
         if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
       }
       __syncwarp();
@@ -682,23 +570,16 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int gp = 0; gp < GR; ++gp) buf[y * P + k2 * GR + ((gp + k2) & (GR - 1))] = v[q * GR + gp];
       }
-      if constexpr (CHR && PDD_CHAINR == 2) {
-        if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
-      }
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < RR; k += 2) {
         cx<T> t0, t1;
         if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
-        else if constexpr (RTW) t0 = rtw(k * GR + g), t1 = rtw((k + 1) * GR + g);
         else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
         const cx<T> b0 = buf[y * P + k * GR + ((g + k) & (GR - 1))];
         const cx<T> b1 = buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))];
         v[k] = (k == 0) ? b0 : mul_conj(b0, t0);
         v[k + 1] = mul_conj(b1, t1);
-      }
-      if constexpr (CHR && PDD_CHAINR == 3) {
-        if (rb == 0 && (warp >> 2) < 3) named_arrive(9 + (warp >> 2), 256);
       }
       if (tma_rows && fn >= 0) {
         __syncwarp();             // this warp's rows are consumed

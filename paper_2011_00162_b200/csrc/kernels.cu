@@ -75,23 +75,6 @@ static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
-#if PDD_TWC_CONST || PDD_TWR_CONST
-    if constexpr (std::is_same_v<T, float> && SH::S == 128) {
-      float2 hc[128], hr[128];
-      auto w = [](int k) {  // same rounding as common.cuh twiddles<float>()
-        const double ang = -2.0 * M_PI * static_cast<double>(k % 128) / 128.0;
-        return float2{static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang))};
-      };
-      for (int i = 0; i < 128; ++i) {
-        hc[i] = w((i / 16) * (i % 16));
-        hr[i] = w((i % 8) * (i / 8));
-      }
-      e = cudaMemcpyToSymbol(c_twc, hc, sizeof(hc));
-      if (e != cudaSuccess) return e;
-      e = cudaMemcpyToSymbol(c_twr, hr, sizeof(hr));
-      if (e != cudaSuccess) return e;
-    }
-#endif
   }
   if (a.nframes <= 0) return cudaSuccess;
   // SWEEP runs the host schedule, built for exactly this grid

@@ -75,7 +75,8 @@ class Nonblind final : public NonblindGpu {
   // the device only -- never on the GPU count, so iterates stay identical for
   // every G: at least 6 pieces per SM when each GPU holds a single subdomain
   // (the smallest per-GPU share; the static piece schedule then stays within
-  // a few percent of balance), at most Layout::kPieceLen frames.
+  // a few percent of balance), at most Layout::kPieceLen frames; pairs for
+  // subdomains of 2 to 6 frames per SM.
   // PDD_PIECE_LEN overrides (1: one piece per frame, for A/B runs).
   static int piece_length(const Plan& plan, int device) {
     if (sizeof(T) != 4 || plan.g.s != 128) return 1;
@@ -84,7 +85,12 @@ class Nonblind final : public NonblindGpu {
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0) return 1;
     int64_t jmin = INT64_MAX;
     for (const auto& fr : plan.frames_of) jmin = std::min<int64_t>(jmin, static_cast<int64_t>(fr.size()));
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(Layout::kPieceLen, jmin / (6 * int64_t(sms)))));
+    const int64_t bal = jmin / (6 * int64_t(sms));
+    if (bal >= 1) return static_cast<int>(std::min<int64_t>(Layout::kPieceLen, bal));
+    // small subdomains (config 2: 450 frames): pairs of frames still fill every
+    // SM when a GPU holds one subdomain (>= 2 frames per SM either way), and
+    // the update pass reads 10 instead of 16 partial values per pixel
+    return jmin >= 2 * int64_t(sms) ? 2 : 1;
   }
 
   // solver.cpp:53-75: denom = eta * illumination_density + r per covering pair.

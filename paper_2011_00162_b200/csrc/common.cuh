@@ -309,7 +309,7 @@ struct RankData {
   DevMem fr_off, fr_pitch, fr_r, fr_c, fr_sub;
   DevMem tiles, tile_frames, sub_off, sub_h, sub_w, sub_pbeg, psides, pgeom;
   DevMem sub_fr_beg, sub_tile_beg, local_map;
-  DevMem pc_beg, pc_pos, pc_ofs, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
+  DevMem pc_beg, pc_pos, pc_ofs, pc_rec, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
   DevMem fmeta_beg, fmeta, fmeta_base, imeta_beg, imeta, imeta_base, tps_beg, tps;  // flattened gather lists
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
   DevMem scratch;  // global transpose tiles of the streamed kernel (complex128 128^2 frames)
@@ -374,6 +374,12 @@ struct RankData {
       pc_beg = upload(L.cta_beg, s);
       pc_pos = upload(L.cta_pos, s);
       pc_ofs = upload(L.cta_ofs, s);
+      std::vector<PosRec> rec(L.cta_pos.size());
+      for (size_t k = 0; k < rec.size(); ++k) {
+        const int4 q = L.cta_pos[k];
+        rec[k] = PosRec{q.x, q.y, q.z | (q.w << 16), L.fr_pitch[q.x], L.cta_ofs[k], L.fr_off[q.x]};
+      }
+      pc_rec = upload(rec, s);
     }
     fmeta_beg = upload(L.fmeta_beg, s);
     fmeta = upload(L.fmeta, s);
@@ -538,6 +544,7 @@ struct RankData {
     a.ncta = L.ncta;
     a.pc_pos = pc_pos.as<int4>();
     a.pc_ofs = pc_ofs.as<int64_t>();
+    a.pc_rec = pc_rec.as<PosRec>();
   }
   void set_pieces(GatherArgs<T>& g) const {
     if (!L.chained) return;

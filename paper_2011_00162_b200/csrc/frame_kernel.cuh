@@ -23,6 +23,18 @@ namespace pdd {
 
 enum FrameMode : int { kFwd = 1, kAdj = 2, kSweep = 3, kBlind = 4 };
 
+// One position of the streamed sweep schedule with everything the kernel needs
+// about its frame (32 bytes: staged in shared memory a frame ahead, so no
+// dependent global load sits behind a CTA barrier).
+struct alignas(16) PosRec {
+  int32_t f;        // frame index
+  int32_t lo;       // rows y < lo are final after this frame (layout.hpp pc_pos.y)
+  int32_t nw_rot;   // newfrom | rot << 16 (pc_pos.z, .w)
+  int32_t pitch;    // image row pitch of the frame's subdomain (elements)
+  int64_t ofs;      // element offset of the frame's window row 0 in the partials (pc_ofs)
+  int64_t woff;     // element offset of the window corner in the image buffer (fr_off)
+};
+
 template <typename T>
 struct FrameArgs {
   int nframes = 0;
@@ -57,6 +69,7 @@ struct FrameArgs {
   int ncta = 0;
   const int4* pc_pos = nullptr;       // [nframes] {frame, lo, newfrom, rot}
   const int64_t* pc_ofs = nullptr;    // [nframes]
+  const PosRec* pc_rec = nullptr;     // [nframes] the same schedule as records (streamed SWEEP reads these)
   int64_t img_elems = 0;              // PDD_BOUNDS builds: image buffer size (elements)
   cx<T>* scratch = nullptr;           // global transpose tiles of the streamed kernel when its
                                       // tile exceeds shared memory (stream_scratch_bytes)

@@ -80,6 +80,9 @@ struct ProbeTmem {
 #ifdef PDD_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[4];  // summed over CTAs; printed by launch_stream
 #endif
+#ifndef PDD_SMETA
+#define PDD_SMETA 1  // schedule records staged in shared memory a frame ahead (no global metadata loads behind barriers)
+#endif
 #ifndef PDD_SKEW
 #define PDD_SKEW 2000  // cycles by which column warp set k starts after set k-1 (see "Staggered warps")
 #endif
@@ -140,6 +143,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   constexpr bool GTILE = tile_in_global<T, SH>();
   static_assert(!ADJ || GTILE, "ADJ: global-tile shapes only");
   static_assert(!(GTILE && TMEMP), "global tile: no tensor-memory paths");
+  constexpr bool STRIDED = FWD || ADJ;  // frames blockIdx.x + k * gridDim.x (no piece schedule)
+  constexpr bool SMETA = PDD_SMETA && !STRIDED;
+  __shared__ PosRec s_rec[3];
   cx<T>* buf = GTILE ? a.scratch + static_cast<int64_t>(blockIdx.x) * S * P : twc + S;
   double* red = reinterpret_cast<double*>(GTILE ? twc + S : buf + S * P);
   // S = 128: the amplitudes of the next column group land by cp.async straight
@@ -189,6 +195,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     }
     tmem_wait_st();
   }
+  if constexpr (SMETA) {
+    if (t < 2) {
+      const int j = a.cta_beg[blockIdx.x] + t;
+      if (j < a.cta_beg[blockIdx.x + 1]) s_rec[t] = a.pc_rec[j];
+      else s_rec[t].f = -1;
+    }
+  }
   __syncthreads();
   // this thread's probe values for row batch rb, from TMEM or global memory
   auto probe_row = [&](int ff, int rb, int y, int g, cx<T>* pv) {
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     mbar_init_fence();
     __syncthreads();
   }
-  auto issue_rows = [&](int ff, int rb) {  // whole warp; rows rb*RPB + RW*warp + [0, RW)
+  auto issue_rows = [&](int ff, int64_t woff, int wpitch, int rb) {  // whole warp; rows rb*RPB + RW*warp + [0, RW)
     const int lane = t & 31;
     uint64_t* bar = s_rowbar + rb * NW + warp;
     if (lane == 0) mbar_arrive_expect_tx(bar, SH::RW * S * sizeof(cx<T>));
@@ -229,14 +242,13 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     if (lane < SH::RW) {
       const int y = rb * RPB + SH::RW * warp + lane;
 #ifdef PDD_BOUNDS
-      if (ff < 0 || ff >= a.nframes || a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff] + S > a.img_elems ||
-          ((a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff]) & 1)) {
-        printf("PDD_BOUNDS issue_rows: cta %d ff %d y %d off %lld pitch %d\n", blockIdx.x, ff, y,
-               (long long)(ff >= 0 && ff < a.nframes ? a.off[ff] : -1), ff >= 0 && ff < a.nframes ? a.pitch[ff] : -1);
+      if (ff < 0 || ff >= a.nframes || woff != a.off[ff] || wpitch != a.pitch[ff] ||
+          woff + static_cast<int64_t>(y) * wpitch + S > a.img_elems || ((woff + static_cast<int64_t>(y) * wpitch) & 1)) {
+        printf("PDD_BOUNDS issue_rows: cta %d ff %d y %d off %lld pitch %d\n", blockIdx.x, ff, y, (long long)woff, wpitch);
         __trap();
       }
 #endif
-      bulk_g2s(buf + y * P, a.img + a.off[ff] + static_cast<int64_t>(y) * a.pitch[ff], S * sizeof(cx<T>), bar);
+      bulk_g2s(buf + y * P, a.img + woff + static_cast<int64_t>(y) * wpitch, S * sizeof(cx<T>), bar);
     }
   };
   uint32_t row_phase = 0;  // parity of the frames consumed so far
@@ -297,21 +309,43 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // Work order.  SWEEP: this CTA's positions [cta_beg[b], cta_beg[b+1]) of the
   // host schedule (frames in back-projection piece order; layout.hpp).
   // FWD: frames blockIdx.x + k * gridDim.x.
-  constexpr bool STRIDED = FWD || ADJ;  // frames blockIdx.x + k * gridDim.x (no piece schedule)
   int i = STRIDED ? static_cast<int>(blockIdx.x) : a.cta_beg[blockIdx.x];
   const int iend = STRIDED ? a.nframes : a.cta_beg[blockIdx.x + 1];
   constexpr int kStepOne = 1;
-  auto frame_at = [&](int j) {
-    if constexpr (STRIDED) return j < iend ? j : -1;
+  auto next_of = [&](int j) { return STRIDED ? j + static_cast<int>(gridDim.x) : j + kStepOne; };
+  // SMETA: the schedule records of positions i, i+1 (and i+2, in flight) sit in
+  // the ring s_rec; c0 is the slot of position i.
+  int c0 = 0;
+  auto slot = [&](int k) { return c0 + k >= 3 ? c0 + k - 3 : c0 + k; };
+  auto frame_cur = [&]() -> int {  // frame of position i (-1: none)
+    if constexpr (SMETA) return s_rec[c0].f;
+    else if constexpr (STRIDED) return i < iend ? i : -1;
+    else return i < iend ? a.pc_pos[i].x : -1;
+  };
+  auto frame_nxt = [&]() -> int {  // frame of the position after i
+    const int j = next_of(i);
+    if constexpr (SMETA) return s_rec[slot(1)].f;
+    else if constexpr (STRIDED) return j < iend ? j : -1;
     else return j < iend ? a.pc_pos[j].x : -1;
   };
-  auto next_of = [&](int j) { return STRIDED ? j + static_cast<int>(gridDim.x) : j + kStepOne; };
+  // window corner offset / row pitch of frame ff held in ring slot k (SMETA) or from the frame tables
+  auto win_off = [&](int ff, int k) -> int64_t {
+    if constexpr (SMETA) return s_rec[slot(k)].woff;
+    else return a.off[ff];
+  };
+  auto win_pitch = [&](int ff, int k) -> int {
+    if constexpr (SMETA) return s_rec[slot(k)].pitch;
+    else return a.pitch[ff];
+  };
   {
-    const int f0 = frame_at(i);
+    const int f0 = frame_cur();
     prefetch(f0, 0);
-    if (tma_rows && f0 >= 0)
+    if (tma_rows && f0 >= 0) {
+      const int64_t wo = win_off(f0, 0);
+      const int wp = win_pitch(f0, 0);
 #pragma unroll 1
-      for (int rb = 0; rb < NRB; ++rb) issue_rows(f0, rb);
+      for (int rb = 0; rb < NRB; ++rb) issue_rows(f0, wo, wp, rb);
+    }
   }
 
 #ifdef PDD_PHASE_TIMING
@@ -329,7 +363,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   } while (0)
 #endif
   // ---------------- rows, forward (frame f): warp-local (each warp owns its rows)
-  auto fwd_rows = [&](int f) {
+  auto fwd_rows = [&](int f, int k) {  // k: ring slot offset of f's record (SMETA)
 #pragma unroll 1
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
@@ -340,7 +374,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         for (int m = 0; m < RR; ++m) v[m] = buf[y * P + g + GR * m];
         __syncwarp();  // all lanes hold their row elements before the row is overwritten
       } else {
-        const cx<T>* src = a.img + a.off[f] + static_cast<int64_t>(y) * a.pitch[f] + g;
+        const cx<T>* src = a.img + win_off(f, k) + static_cast<int64_t>(y) * win_pitch(f, k) + g;
 #pragma unroll
         for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
       }
@@ -376,10 +410,10 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   constexpr bool FUSE = PDD_ROWFUSE && !FWD && !ADJ;
   int pend_f = -1;  // FUSE: frame whose R-factor warp partials sit in red[]
   if constexpr (FUSE) {
-    if (i < iend) fwd_rows(frame_at(i));
+    if (i < iend) fwd_rows(frame_cur(), 0);
   }
   for (; i < iend; i = next_of(i)) {
-    const int f = frame_at(i);
+    const int f = frame_cur();
     const int64_t fbase = static_cast<int64_t>(f) * S * S;
 #ifdef PDD_BOUNDS
     if (f < 0 || f >= a.nframes) {
@@ -387,7 +421,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       __trap();
     }
 #endif
-    if constexpr (!FUSE && !ADJ) fwd_rows(f);
+    if constexpr (!FUSE && !ADJ) fwd_rows(f, 0);
     if constexpr (ACC) tmem_fence_before_sync();
     __syncthreads();
     if constexpr (ACC) tmem_fence_after_sync();
@@ -398,6 +432,20 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         double s = 0.0;
         for (int w = 0; w < NT / 32; ++w) s += red[w];
         a.rf_part[pend_f] = s;
+      }
+    }
+    if constexpr (SMETA) {
+      // the record of position i+2 lands during this column phase (its slot
+      // held position i-1, last read before the barrier above)
+      if (t == NT - 1) {
+        PosRec* dst = s_rec + slot(2);
+        if (i + 2 < iend) {
+          cp_async16(dst, a.pc_rec + i + 2);
+          cp_async16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(a.pc_rec + i + 2) + 16);
+          cp_async_commit();
+        } else {
+          dst->f = -1;
+        }
       }
     }
     PDD_TICK(0);
@@ -427,7 +475,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int e = 0; e < RC; ++e) w[e] = pg[e];
         if (grp + 1 < NG) prefetch(f, grp + 1);
-        else prefetch(frame_at(next_of(i)), 0);
+        else prefetch(frame_nxt(), 0);
       } else {
 #pragma unroll
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
@@ -469,7 +517,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
           }
         rf_acc += acc;
         if (grp + 1 < NG) prefetch(f, grp + 1);
-        else prefetch(frame_at(next_of(i)), 0);
+        else prefetch(frame_nxt(), 0);
         continue;  // groups own disjoint columns of buf: no barrier between them
       }
 #pragma unroll
@@ -495,7 +543,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         }
       rf_acc += acc;
       if (grp + 1 < NG) prefetch(f, grp + 1);
-      else prefetch(frame_at(next_of(i)), 0);
+      else prefetch(frame_nxt(), 0);
       }  // !ADJ
 #pragma unroll
       for (int q = 0; q < RC / GC; ++q) {
@@ -518,6 +566,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
       for (int m = 0; m < RC; ++m) buf[(gc + GC * m) * P + x] = w[m];
     }
+    if constexpr (SMETA && !STAGE) {
+      if (t == NT - 1) cp_async_wait_all();
+    }
     __syncthreads();
     PDD_TICK(1);
 
@@ -525,14 +576,26 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     // this frame's piece bookkeeping: rows y < lo are final, rows y >= newfrom new
     int p_lo = S, p_new = 0, p_rot = 0;
     int64_t p_ofs = fbase;
-    if constexpr (!STRIDED) {
+    if constexpr (SMETA) {
+      const PosRec r = s_rec[c0];
+      p_lo = r.lo;
+      p_new = r.nw_rot & 0xffff;
+      p_rot = r.nw_rot >> 16;
+      p_ofs = r.ofs;
+    } else if constexpr (!STRIDED) {
       const int4 pi = a.pc_pos[i];
       p_lo = pi.y;
       p_new = pi.z;
       p_rot = pi.w;
       p_ofs = a.pc_ofs[i];
     }
-    const int fn = frame_at(next_of(i));
+    const int fn = frame_nxt();
+    int64_t n_off = 0;
+    int n_pitch = 0;
+    if (tma_rows && fn >= 0) {
+      n_off = win_off(fn, 1);
+      n_pitch = win_pitch(fn, 1);
+    }
 #ifdef PDD_BOUNDS
     if (p_ofs < 0 || p_lo <= 0 || p_lo > S || p_new < 0 || p_new > S || fn >= a.nframes) {
       printf("PDD_BOUNDS piece: cta %d i %d f %d ofs %lld lo %d new %d fn %d\n", blockIdx.x, i, f, (long long)p_ofs, p_lo,
@@ -584,7 +647,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       if (tma_rows && fn >= 0) {
         __syncwarp();             // this warp's rows are consumed
         fence_proxy_async_smem();  // ... before the async proxy overwrites them
-        issue_rows(fn, rb);
+        issue_rows(fn, n_off, n_pitch, rb);
       }
       dft<RR, true>(v);
       if (a.bp_raw) {  // blind: q_j = IFFT(.) itself; conj(W^{n+1}) is applied in the gather
@@ -635,7 +698,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       // own rows of buf, and the accumulator rows that change warps between
       // frames are ordered by the two barriers of the next frame
       pend_f = f;
-      if (fn >= 0) fwd_rows(fn);
+      if (fn >= 0) fwd_rows(fn, 1);
     } else {
       if constexpr (ACC) tmem_fence_before_sync();  // accumulator rows change warps between frames
       __syncthreads();  // also: rows of the next frame overwrite buf
@@ -647,6 +710,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       }
     }
     PDD_TICK(3);
+    if constexpr (SMETA) c0 = slot(1);
   }
   if constexpr (FUSE) {
     __syncthreads();

@@ -455,13 +455,24 @@ def bench_ours(args, cfg, base, rank, world, local, dist):
         torch.cuda.empty_cache()
         amp_np = host.numpy()
         nccl_id = None if replicas else fresh_nccl_id(dist, rank, world)  # an id bootstraps one communicator
-        t_e2e, res, n_loc = e2e_solve(cfg, plan, probe, amp_np, local, srank, sworld, nccl_id, dist, w0=w0)
+        # three full solves, each with its own upload and downloads; the median is
+        # reported (the first one after the timed solver released its ~30 GB
+        # re-maps pooled device memory) and all three are listed
+        t_all = []
+        for rep in range(3):
+            if rep > 0 and not replicas:
+                nccl_id = fresh_nccl_id(dist, rank, world)
+            t_rep, res, n_loc = e2e_solve(cfg, plan, probe, amp_np, local, srank, sworld, nccl_id, dist, w0=w0)
+            t_all.append(t_rep)
+        t_e2e = sorted(t_all)[1]
         g = plan.geometry
         h2d = j_local * s * s * 4 + probe.nbytes
         d2h = n_loc * 16 + (g.image_height * g.image_width * 16 if sworld == 1 else 0) + res.iterations * 24
         line["e2e"] = {"value": copies * J * res.iterations / t_e2e, "unit": base["unit"], "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "iterations_per_step": res.iterations,
-                       "input": "float32 amplitudes, page-locked host buffer", "process": "warm (second solve)",
+                       "input": "float32 amplitudes, page-locked host buffer",
+                       "process": "warm (solves 2-4 of the process; median of three)",
+                       "solve_seconds": [round(x, 4) for x in t_all],
                        "timer": "host wall clock around synchronous C-ABI calls (create+upload, run, download)"}
         if rank == 0 and world == 1:
             # (2) the reference's own input type: float64 intensities (FrameStack, scan.hpp:38-43),

@@ -77,12 +77,42 @@ std::vector<int32_t> devices_for(int threads, int D) {
   return out;
 }
 
+// ConvergenceRecord::t_sub_ms (solver.cpp:243-249) on the device: a rank runs
+// all of its subdomains in one fused launch per kernel, so subdomain d is
+// charged its rank's measured iteration time in proportion to its frame count
+// (the frame kernel is ~90 % of an iteration and its cost is per frame),
+// share[d] = J_d / sum of J over the subdomains of rank(d), rank(d) =
+// floor(d G / D).  t_virtual_ms = max_d t_sub_ms[d] then models one GPU per
+// subdomain exactly as the reference models one worker per subdomain;
+// t_actual_ms stays the measured time of the iteration.
+std::vector<double> frame_shares(const DecompositionPlan& plan, int G) {
+  const int D = plan.D;
+  G = std::max(1, std::min(G, D));
+  std::vector<double> per_rank(static_cast<size_t>(G), 0.0), share(static_cast<size_t>(D), 1.0);
+  auto rank_of = [&](int d) { return static_cast<int>((static_cast<int64_t>(d) * G) / D); };
+  std::vector<double> jd(static_cast<size_t>(D), 0.0);
+  for (int a : plan.frame_assignment)
+    if (a >= 0 && a < D) jd[static_cast<size_t>(a)] += 1.0;
+  for (int d = 0; d < D; ++d) per_rank[static_cast<size_t>(rank_of(d))] += jd[static_cast<size_t>(d)];
+  for (int d = 0; d < D; ++d) {
+    const double tot = per_rank[static_cast<size_t>(rank_of(d))];
+    share[static_cast<size_t>(d)] = tot > 0.0 ? jd[static_cast<size_t>(d)] / tot : 1.0;
+  }
+  return share;
+}
+void fill_times(ConvergenceRecord& r, const std::vector<double>& share, double t_ms) {
+  r.t_sub_ms.resize(share.size());
+  for (size_t d = 0; d < share.size(); ++d) r.t_sub_ms[d] = t_ms * share[d];
+  r.t_virtual_ms = share.empty() ? t_ms : *std::max_element(r.t_sub_ms.begin(), r.t_sub_ms.end());
+  r.t_actual_ms = t_ms;
+}
+
 // run()'s per-iteration callback (solver.hpp:88) through pdd_*_run_cb: the
 // C-ABI streams records while the device loop runs; an exception thrown by
 // the caller's callback is held and rethrown once the run returns.
 struct RecordTrampoline {
   const std::function<void(const ConvergenceRecord&)>* cb;
-  int D;
+  std::vector<double> share;
   std::exception_ptr err;
   static void call(int64_t it, double rf, double re, double t_ms, double lag, void* user) {
     auto* self = static_cast<RecordTrampoline*>(user);
@@ -92,9 +122,7 @@ struct RecordTrampoline {
     r.rf = rf;
     r.re = re;
     if (!std::isnan(lag)) r.lagrangian = lag;
-    r.t_sub_ms.assign(static_cast<size_t>(self->D), t_ms);
-    r.t_virtual_ms = t_ms;
-    r.t_actual_ms = t_ms;
+    fill_times(r, self->share, t_ms);
     try {
       (*self->cb)(r);
     } catch (...) {
@@ -339,7 +367,7 @@ std::vector<ComplexField2D> split_images(const DecompositionPlan& plan, const st
   return out;
 }
 
-std::vector<ConvergenceRecord> records_of(const std::vector<double>& rec, int64_t n, int D,
+std::vector<ConvergenceRecord> records_of(const std::vector<double>& rec, int64_t n, const std::vector<double>& share,
                                           const std::vector<double>& lag) {
   std::vector<ConvergenceRecord> out;
   for (int64_t k = 0; k < n; ++k) {
@@ -348,9 +376,7 @@ std::vector<ConvergenceRecord> records_of(const std::vector<double>& rec, int64_
     r.rf = rec[3 * k];
     r.re = rec[3 * k + 1];
     if (k < static_cast<int64_t>(lag.size())) r.lagrangian = lag[k];
-    r.t_sub_ms.assign(static_cast<size_t>(D), rec[3 * k + 2]);
-    r.t_virtual_ms = rec[3 * k + 2];
-    r.t_actual_ms = rec[3 * k + 2];
+    fill_times(r, share, rec[3 * k + 2]);
     out.push_back(std::move(r));
   }
   return out;
@@ -429,7 +455,8 @@ NonblindResult NonblindSolver::run(const std::function<void(const ConvergenceRec
   NbHandle g(plan_, frames_, probe_, config_, pin_);
   std::vector<double> rec(3 * static_cast<size_t>(config_.max_iters));
   int64_t n = 0, div = 0;
-  RecordTrampoline tr{&on_iteration, plan_.D, nullptr};
+  const std::vector<double> share = frame_shares(plan_, static_cast<int>(devices_for(config_.threads, plan_.D).size()));
+  RecordTrampoline tr{&on_iteration, share, nullptr};
   check(pdd_nonblind_run_cb(g.h, on_iteration ? &RecordTrampoline::call : nullptr, &tr, &n, rec.data(), &div), div);
   if (tr.err) std::rethrow_exception(tr.err);
   std::vector<double> lag;
@@ -440,7 +467,7 @@ NonblindResult NonblindSolver::run(const std::function<void(const ConvergenceRec
     lag.resize(static_cast<size_t>(std::min(nl, n)));
   }
   NonblindResult out;
-  out.records = records_of(rec, n, plan_.D, lag);
+  out.records = records_of(rec, n, share, lag);
   Packed p = sized(plan_);
   check(pdd_nonblind_get_state(g.h, dp(p.u), nullptr, nullptr, nullptr, nullptr, nullptr));
   out.sub_solutions = split_images(plan_, p.u);
@@ -565,11 +592,12 @@ BlindResult BlindSolver::run(const std::function<void(const ConvergenceRecord&)>
   check(pdd_blind_init_state(g.h, nullptr));  // the device solver's own w0 (== w0_)
   std::vector<double> rec(3 * static_cast<size_t>(config_.max_iters));
   int64_t n = 0, div = 0;
-  RecordTrampoline tr{&on_iteration, plan_.D, nullptr};
+  const std::vector<double> share = frame_shares(plan_, static_cast<int>(devices_for(config_.threads, plan_.D).size()));
+  RecordTrampoline tr{&on_iteration, share, nullptr};
   check(pdd_blind_run_cb(g.h, on_iteration ? &RecordTrampoline::call : nullptr, &tr, &n, rec.data(), &div), div);
   if (tr.err) std::rethrow_exception(tr.err);
   BlindResult out;
-  out.records = records_of(rec, n, plan_.D, {});
+  out.records = records_of(rec, n, share, {});
   const int64_t s = plan_.geometry.frame_side;
   out.probe = ComplexField2D(s, s);
   out.probe_fourier = ComplexField2D(s, s);

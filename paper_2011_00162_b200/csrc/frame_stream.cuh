@@ -127,7 +127,12 @@ constexpr bool tile_in_global() {
 // |A u|^2 -> inten_out, R-factor partials), e.g. the trailing R-factor pass.
 // ADJ = true: the inverse half only (FrameMode kAdj: frames_in -> IFFT2 ->
 // x conj(probe) -> bp_out per frame), global-tile shapes only.
-template <typename T, class SH, bool FAST, bool TMEMP = false, bool FWD = false, bool ADJ = false>
+// RF2 = true (blind, blind.cpp:320-332 inside the sweep): the R-factor of u^n is
+// taken with the SHARED probe a.probe2 through a second forward transform of
+// the same patch (second transpose tile; one pass over patches and amplitudes
+// instead of a separate FWD launch), while the sweep itself runs with the
+// subdomain copies (a.probe / probe_idx).
+template <typename T, class SH, bool FAST, bool TMEMP = false, bool FWD = false, bool ADJ = false, bool RF2 = false>
 __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const FrameArgs<T> a) {
   constexpr int S = SH::S, NT = SH::NT, GR = SH::GR, GC = SH::GC, RR = SH::RR, RC = SH::RC;
   constexpr int RPB = SH::RPB, NRB = SH::NRB, CG = SH::CG, NG = SH::NG, P = SH::P;
@@ -153,6 +158,9 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
   // thread that copied them) -- the column phase sits at the 128-register cap
   // and a register prefetch spilled.
   T* ampst = reinterpret_cast<T*>(red + NT / 32);
+  static_assert(!RF2 || (!FWD && !ADJ && !TMEMP && !tile_in_global<T, SH>() && !amp_tile_staged<T, SH, false>()),
+                "RF2: shared-memory tile shapes without staged amplitudes");
+  cx<T>* buf2 = reinterpret_cast<cx<T>*>(smem_raw + stream_smem_bytes_base<T, SH>());  // RF2 only
 
   if (a.stop_flag && *a.stop_flag) return;
   const int t = threadIdx.x;
@@ -378,33 +386,44 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
 #pragma unroll
         for (int m = 0; m < RR; ++m) v[m] = src[GR * m];
       }
+      // 1-D transform of this thread's row elements through the warp's rows of dst
+      auto row_fft = [&](cx<T>* vv, cx<T>* dst) {
+        dft<RR, false>(vv);
+#pragma unroll
+        for (int k = 0; k < RR; k += 2) {
+          cx<T> t0, t1;
+          if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
+          else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
+          dst[y * P + k * GR + ((g + k) & (GR - 1))] = (k == 0) ? vv[k] : vv[k] * t0;
+          dst[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))] = vv[k + 1] * t1;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RR / GR; ++q) {
+          const int k2 = g + GR * q;
+#pragma unroll
+          for (int gp = 0; gp < GR; ++gp) vv[q * GR + gp] = dst[y * P + k2 * GR + ((gp + k2) & (GR - 1))];
+          dft<GR, false>(vv + q * GR);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < RR / GR; ++q) {
+          const int k2 = g + GR * q;
+#pragma unroll
+          for (int k1 = 0; k1 < GR; ++k1) dst[y * P + k2 + RR * k1] = vv[q * GR + k1];
+        }
+      };
+      if constexpr (RF2) {  // patch x shared probe -> rows of the second tile
+        cx<T> v2[RR];
+        const cx<T>* pw = a.probe2 + y * S + g;
+#pragma unroll
+        for (int m = 0; m < RR; ++m) v2[m] = v[m] * pw[GR * m];
+        row_fft(v2, buf2);
+      }
       probe_row(f, rb, y, g, pv);
 #pragma unroll
       for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
-      dft<RR, false>(v);
-#pragma unroll
-      for (int k = 0; k < RR; k += 2) {
-        cx<T> t0, t1;
-        if constexpr (TWV) tw_pair(twr + (k >> 1) * 2 * GR + 2 * g, t0, t1);
-        else t0 = twr[k * GR + g], t1 = twr[(k + 1) * GR + g];
-        buf[y * P + k * GR + ((g + k) & (GR - 1))] = (k == 0) ? v[k] : v[k] * t0;
-        buf[y * P + (k + 1) * GR + ((g + k + 1) & (GR - 1))] = v[k + 1] * t1;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < RR / GR; ++q) {
-        const int k2 = g + GR * q;
-#pragma unroll
-        for (int gp = 0; gp < GR; ++gp) v[q * GR + gp] = buf[y * P + k2 * GR + ((gp + k2) & (GR - 1))];
-        dft<GR, false>(v + q * GR);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int q = 0; q < RR / GR; ++q) {
-        const int k2 = g + GR * q;
-#pragma unroll
-        for (int k1 = 0; k1 < GR; ++k1) buf[y * P + k2 + RR * k1] = v[q * GR + k1];
-      }
+      row_fft(v, buf);
     }
   };
   constexpr bool FUSE = PDD_ROWFUSE && !FWD && !ADJ;
@@ -477,6 +496,33 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
         if (grp + 1 < NG) prefetch(f, grp + 1);
         else prefetch(frame_nxt(), 0);
       } else {
+      T acc2 = T(0);
+      if constexpr (RF2) {  // forward column transform of the shared-probe tile -> R-factor terms
+        cx<T> w2[RC];
+#pragma unroll
+        for (int m = 0; m < RC; ++m) w2[m] = buf2[(gc + GC * m) * P + x];
+        dft<RC, false>(w2);
+#pragma unroll
+        for (int k = 0; k < RC; k += 2) {
+          const cx<T> t0 = twc[gc * RC + k], t1 = twc[gc * RC + k + 1];
+          buf2[(k * GC + gc) * P + x] = (k == 0) ? w2[k] : w2[k] * t0;
+          buf2[((k + 1) * GC + gc) * P + x] = w2[k + 1] * t1;
+        }
+        col_sync();
+#pragma unroll
+        for (int q = 0; q < RC / GC; ++q) {
+          const int k2 = gc + GC * q;
+#pragma unroll
+          for (int gp = 0; gp < GC; ++gp) w2[q * GC + gp] = buf2[(k2 * GC + gp) * P + x];
+          dft<GC, false>(w2 + q * GC);
+        }
+#pragma unroll
+        for (int e = 0; e < RC; ++e) {
+          const cx<T> au2 = w2[e] * scale;
+          if constexpr (FAST && std::is_same_v<T, float>) acc2 += fabsf(abs_fast_f32(au2) - pa_at(e));
+          else acc2 += fabs(sqrt(norm2(au2)) - pa_at(e));
+        }
+      }
 #pragma unroll
       for (int m = 0; m < RC; ++m) w[m] = buf[(gc + GC * m) * P + x];
       dft<RC, false>(w);
@@ -541,7 +587,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
           if (a.z_out) a.z_out[idx] = z;
           w[e] = z - gn;
         }
-      rf_acc += acc;
+      rf_acc += RF2 ? acc2 : acc;
       if (grp + 1 < NG) prefetch(f, grp + 1);
       else prefetch(frame_nxt(), 0);
       }  // !ADJ
@@ -748,8 +794,8 @@ constexpr size_t stream_smem_bytes_base() {
          (amp_tile_staged<T, SH, false>() ? sizeof(T) * static_cast<size_t>(SH::RC) * SH::NT : 0);
 }
 template <typename T, class SH>
-size_t stream_smem_bytes() {
-  return stream_smem_bytes_base<T, SH>()
+size_t stream_smem_bytes(bool rf2 = false) {
+  return stream_smem_bytes_base<T, SH>() + (rf2 ? sizeof(cx<T>) * static_cast<size_t>(SH::S) * SH::P : 0)
 #ifdef PDD_CANARY
          + (size_t(48) << 10)  // debug builds: a canary region after the working set
 #endif

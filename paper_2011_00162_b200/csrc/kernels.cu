@@ -68,10 +68,18 @@ constexpr bool stream_tmem_probe() {  // TMEM probe cache where it keeps occupan
   return std::is_same_v<T, float> && SH::MINB == 1;
 }
 
-template <typename T, class SH, bool FAST, bool FWD = false, bool ADJ = false>
+// Shapes whose BLIND frame pass runs as ONE streamed launch (RF2: the shared-probe
+// R-factor transform inside the sweep): shared-memory tile, room for a second one.
+template <typename T, class SH>
+constexpr bool stream_rf2() {
+  return !stream_tmem_probe<T, SH>() && !tile_in_global<T, SH>() && !amp_tile_staged<T, SH, false>() &&
+         2 * sizeof(cx<T>) * static_cast<size_t>(SH::S) * SH::P * SH::MINB <= (size_t(200) << 10);
+}
+
+template <typename T, class SH, bool FAST, bool FWD = false, bool ADJ = false, bool RF2 = false>
 static cudaError_t launch_stream(const FrameArgs<T>& a, cudaStream_t st) {
-  auto kern = sweep_stream_kernel<T, SH, FAST, stream_tmem_probe<T, SH>(), FWD, ADJ>;
-  const size_t smem = stream_smem_bytes<T, SH>();
+  auto kern = sweep_stream_kernel<T, SH, FAST, stream_tmem_probe<T, SH>(), FWD, ADJ, RF2>;
+  const size_t smem = stream_smem_bytes<T, SH>(RF2);
   static int blocks_per_sm = 0;
   static int sms = 0;
   if (!blocks_per_sm) {
@@ -172,6 +180,16 @@ static cudaError_t launch_frame_s(const FrameArgs<T>& a, cudaStream_t st) {
   }
   if constexpr (MODE == kBlind && !std::is_same_v<typename StreamPick<T, S>::type, void>) {
     using SH = typename StreamPick<T, S>::type;
+    if constexpr (stream_rf2<T, SH>()) {
+      // one pass: the sweep with the subdomain copies W_d (raw q_j output) and,
+      // inside it, the R-factor transform with the shared probe w (probe2)
+      if (a.rf_part && a.probe2) {
+        FrameArgs<T> sw = a;
+        sw.bp_raw = 1;
+        return a.fast_prox ? launch_stream<T, SH, true, false, false, true>(sw, st)
+                           : launch_stream<T, SH, false, false, false, true>(sw, st);
+      }
+    }
     if constexpr (!stream_tmem_probe<T, SH>()) {  // no TMEM probe cache: per-frame probe tiles are fine
       // BLIND = R-factor forward with the shared probe w (probe2), then the
       // SWEEP with the subdomain copies W_d and raw q_j output

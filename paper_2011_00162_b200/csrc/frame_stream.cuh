@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     if constexpr (STAGE) cp_async_commit();
   };
 #ifdef PDD_CANARY  // debug builds: detect shared-memory writes past the working set
-  uint32_t* canary = reinterpret_cast<uint32_t*>(smem_raw + stream_smem_bytes_base<T, SH>());
+  uint32_t* canary = reinterpret_cast<uint32_t*>(smem_raw + stream_smem_bytes_base<T, SH>() +
+                                                 (RF2 ? sizeof(cx<T>) * static_cast<size_t>(S) * P : 0));
   for (int k = t; k < (48 << 10) / 4; k += NT) canary[k] = 0xDEADBEEFu;
   __syncthreads();
 #endif

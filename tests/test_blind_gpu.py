@@ -29,21 +29,39 @@ def blind_problem(N=96, s=32, step=8, D=2, grid=None, peak=None, seed=5):
     return f, O.plan_stripes(g, D), P.plan_stripes(gp, D)
 
 
-def compare(st, ost, tol):
-    assert rel_l2(st.w, ost.w) < tol, "w"
-    for a, b in zip(st.w_copies, ost.w_copies):
-        assert rel_l2(a, b) < tol, "w_copies"
-    for a, b in zip(st.delta, ost.delta):
-        assert np.linalg.norm(a - b) / np.linalg.norm(ost.w) < tol, "delta"
-    for a, b in zip(st.u, ost.u):
-        assert rel_l2(a, b) < tol, "u"
-    for a, b in zip(st.gamma, ost.gamma):
-        assert rel_l2(a, b) < tol, "gamma"
-    for a, b in zip(st.v, ost.v):
-        assert rel_l2(a, b) < tol, "v"
-    for (a0, a1), (b0, b1), v in zip(st.lam, ost.lam, ost.v):
-        assert np.linalg.norm(a0 - b0) / np.linalg.norm(v) < tol, "lambda0"
-        assert np.linalg.norm(a1 - b1) / np.linalg.norm(v) < tol, "lambda1"
+FLOOR_X = 5.0  # as tests/test_configs_gpu.py: blind float32 fields over the bound vs their measured float32 floor
+
+
+def compare(st, ost, tol, f32ref=None):
+    """Fields against their own norm.  f32ref: the numpy restatement evaluated
+    in complex64 at the same point (the float32 floor); a float32 field over
+    the bound must then stay within FLOOR_X of what float32 arithmetic itself
+    makes of the step (z = sign(y) m at near-zero spectral values, Gamma's
+    cancellation)."""
+    def chk(name, a, b, ref=None, scale=None):
+        sc = np.linalg.norm(b) if scale is None else scale
+        e = np.linalg.norm(a - b) / sc
+        if e < tol:
+            return
+        assert ref is not None, f"{name} {e:.3e} >= {tol}"
+        floor = np.linalg.norm(ref - b) / sc
+        assert e <= FLOOR_X * floor, f"{name} {e:.3e} vs float32 floor {floor:.3e}"
+
+    R = f32ref
+    chk("w", st.w, ost.w, None if R is None else R.w)
+    for k, (a, b) in enumerate(zip(st.w_copies, ost.w_copies)):
+        chk("w_copies", a, b, None if R is None else R.w_copies[k])
+    for k, (a, b) in enumerate(zip(st.delta, ost.delta)):
+        chk("delta", a, b, None if R is None else R.delta[k], scale=np.linalg.norm(ost.w))
+    for k, (a, b) in enumerate(zip(st.u, ost.u)):
+        chk("u", a, b, None if R is None else R.u[k])
+    for k, (a, b) in enumerate(zip(st.gamma, ost.gamma)):
+        chk("gamma", a, b, None if R is None else R.gamma[k])
+    for k, (a, b) in enumerate(zip(st.v, ost.v)):
+        chk("v", a, b, None if R is None else R.v[k])
+    for k, ((a0, a1), (b0, b1), v) in enumerate(zip(st.lam, ost.lam, ost.v)):
+        chk("lambda0", a0, b0, None if R is None else R.lam[k][0], scale=np.linalg.norm(v))
+        chk("lambda1", a1, b1, None if R is None else R.lam[k][1], scale=np.linalg.norm(v))
 
 
 @pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-5)])
@@ -59,26 +77,37 @@ def test_blind_setup_and_steps_match_oracle(dtype, tol, D, grid):
     assert rel_l2(gs.initial_probe(), osol.w0) < tol
     assert np.array_equal(gs.support_mask(), osol.mask)
     st, ost = gs.init_state(), osol.init_state()
-    for _ in range(3):
+    fsol = O.BlindSolver(oplan, f, O.BlindConfig(**cfg), precision="f32") if dtype == "f32" else None
+    fst = fsol.init_state() if fsol else None
+    for k in range(3):
         gs.step(st)
         osol.step(ost)
-    compare(st, ost, tol * 10)
+        if fsol:
+            fsol.step(fst)
+        if k == 0:
+            compare(st, ost, tol, fst)  # one sweep: the north-star operator bound
+    compare(st, ost, tol * 10, fst)
 
 
 @pytest.mark.parametrize("N,step,D,grid", [(256, 16, 2, None), (320, 16, None, (2, 2)), (250, 17, 2, None)])
 def test_streamed_blind_frames_match_oracle(N, step, D, grid):
-    """float32 s = 64: the BLIND frame pass runs as two streamed launches (the
-    R-factor forward with w, then the sweep with W_d and raw q_j output)."""
+    """float32 s = 64: the BLIND frame pass runs as ONE streamed launch -- the
+    sweep with W_d (raw q_j output) with the shared-probe R-factor transform
+    inside it (frame_stream.cuh RF2)."""
     f, oplan, plan = blind_problem(N=N, s=64, step=step, D=D or 1, grid=grid, peak=1e4)
     f = fp32_intensity(f)
     cfg = dict(r=5e3)
     gs = P.BlindSolver(plan, f, P.BlindConfig(**cfg), dtype="f32")
     osol = O.BlindSolver(oplan, f, O.BlindConfig(**cfg))
-    st, ost = gs.init_state(), osol.init_state()
-    for _ in range(2):
+    fsol = O.BlindSolver(oplan, f, O.BlindConfig(**cfg), precision="f32")  # the float32 floor
+    st, ost, fst = gs.init_state(), osol.init_state(), fsol.init_state()
+    for k in range(2):
         gs.step(st)
         osol.step(ost)
-    compare(st, ost, 1e-4)
+        fsol.step(fst)
+        if k == 0:
+            compare(st, ost, 1e-5, fst)  # one sweep: the north-star operator bound
+    compare(st, ost, 1e-4, fst)
     res = P.BlindSolver(plan, f, P.BlindConfig(max_iters=5, tol_rf=1e-300, **cfg), dtype="f32").run()
     _, om, oprobe, _, orec = O.BlindSolver(oplan, f, O.BlindConfig(max_iters=5, tol_rf=1e-300, **cfg)).run()
     assert np.max(np.abs(np.array([r.rf for r in res.records]) - [r.rf for r in orec]) /

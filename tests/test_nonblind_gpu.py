@@ -44,25 +44,40 @@ def small_problem(N=128, s=32, step=8, D=2, seed=0, peak=None, grid=None, axis="
     return probe, f, O.plan_stripes(g, D, axis), P.plan_stripes(P.make_raster_scan(N, N, s, step), D, axis)
 
 
-def compare_state(st, ost, tol):
+FLOOR_X = 2.0  # float32 fields over the bound must stay within this factor of the measured float32 floor
+
+
+def compare_state(st, ost, tol, f32ref=None):
+    """Every field against its OWN norm (the north-star bound).  f32ref: the
+    numpy restatement evaluated in complex64 at the same point (oracle
+    precision="f32") -- the float32 floor.  Gamma = y - prox(y) cancels where
+    |y| is close to the measured amplitude, so at 128^2 frames float32
+    arithmetic itself misses the float64 Gamma by ~1.5e-5; a float32 Gamma over
+    the bound is then held to FLOOR_X times that measured floor instead."""
     for a, b in zip(st.u, ost.u):
         assert rel_l2(a, b) < tol, "u"
-    # Gamma = y - prox(y) cancels where |y| is close to the measured amplitude;
-    # a plain float32 implementation (numpy complex64 FFT + prox) misses the
-    # float64 Gamma by 1.5e-5 relative at 128^2 frames, so Gamma is measured
-    # against the scale of the sweep output z it is formed with.
-    for a, b, zb in zip(st.gamma, ost.gamma, ost.z):
-        assert np.linalg.norm(a - b) / max(np.linalg.norm(b), np.linalg.norm(zb)) < tol, "gamma"
+    for k, (a, b) in enumerate(zip(st.gamma, ost.gamma)):
+        nb = np.linalg.norm(b)
+        if nb == 0.0:  # Gamma^0 = 0 exactly
+            assert np.linalg.norm(a) == 0.0, "gamma0"
+            continue
+        e = np.linalg.norm(a - b) / nb
+        if e >= tol:
+            assert f32ref is not None, f"gamma {e:.3e} >= {tol}"
+            floor = np.linalg.norm(f32ref.gamma[k] - b) / nb
+            assert floor >= tol / 2 and e <= FLOOR_X * floor, f"gamma {e:.3e} vs float32 floor {floor:.3e}"
     for a, b in zip(st.z, ost.z):
         assert rel_l2(a, b) < tol, "z"
     for a, b in zip(st.v, ost.v):
         assert rel_l2(a, b) < tol, "v"
-    # Lambda accumulates u - v, a difference of O(1) numbers: its error is
-    # measured against the scale of the overlap iterate it is built from.
+    # Lambda accumulates pi u - v, a difference of O(1) overlap values that agree
+    # to ~1e-3: in float64 it is held to its own norm; in float32 (u carrying
+    # ~1e-6) only relative to the overlap values it is formed from, ||v||.
     for (a0, a1), (b0, b1), v in zip(st.lam, ost.lam, ost.v):
-        scale = np.linalg.norm(v)
-        assert np.linalg.norm(a0 - b0) / scale < tol, "lambda0"
-        assert np.linalg.norm(a1 - b1) / scale < tol, "lambda1"
+        for a, b in ((a0, b0), (a1, b1)):
+            nb = np.linalg.norm(b)
+            scale = nb if (tol <= 1e-8 and nb > 0.0) else np.linalg.norm(v)
+            assert np.linalg.norm(a - b) / scale < tol, "lambda"
 
 
 @pytest.mark.parametrize("dtype,tol", [("f64", 1e-10), ("f32", 1e-5)])
@@ -97,15 +112,18 @@ def test_streamed_sweep_large_frames_matches_oracle(N, s, step, grid):
     f = fp32_intensity(f)
     gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f32")
     osol = O.NonblindSolver(oplan, f, probe, O.NonblindConfig())
-    st, ost = gs.init_state(), osol.init_state()
-    au, oau = [z.copy() for z in st.z], [z.copy() for z in ost.z]
+    fsol = O.NonblindSolver(oplan, f, probe, O.NonblindConfig(), precision="f32")  # the float32 floor
+    st, ost, fst = gs.init_state(), osol.init_state(), fsol.init_state()
+    au, oau, fau = [z.copy() for z in st.z], [z.copy() for z in ost.z], [z.copy() for z in fst.z]
     gs.step(st, au)
     osol.step(ost, oau)
-    compare_state(st, ost, 1e-5)  # one sweep: the north-star operator bound
+    fsol.step(fst, fau)
+    compare_state(st, ost, 1e-5, fst)  # one sweep: the north-star operator bound
     assert abs(gs.r_factor_of(au) - osol.r_factor_of(oau)) <= 1e-5 * osol.r_factor_of(oau)
     gs.step(st, au)
     osol.step(ost, oau)
-    compare_state(st, ost, 1e-4)
+    fsol.step(fst, fau)
+    compare_state(st, ost, 1e-4, fst)
     res = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=6, tol_rf=1e-300), dtype="f32").run()
     _, om, orec = O.NonblindSolver(oplan, f, probe, O.NonblindConfig(max_iters=6, tol_rf=1e-300)).run()
     # N iterations: the north-star float32 bound (perturbations grow ~1.4x
@@ -129,14 +147,17 @@ def test_backprojection_pieces_match_oracle(monkeypatch, piece_len, N, step, gri
     f = fp32_intensity(f)
     gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f32")
     osol = O.NonblindSolver(oplan, f, probe, O.NonblindConfig())
-    st, ost = gs.init_state(), osol.init_state()
-    au, oau = [z.copy() for z in st.z], [z.copy() for z in ost.z]
+    fsol = O.NonblindSolver(oplan, f, probe, O.NonblindConfig(), precision="f32")  # the float32 floor
+    st, ost, fst = gs.init_state(), osol.init_state(), fsol.init_state()
+    au, oau, fau = [z.copy() for z in st.z], [z.copy() for z in ost.z], [z.copy() for z in fst.z]
     gs.step(st, au)
     osol.step(ost, oau)
-    compare_state(st, ost, 1e-5)
+    fsol.step(fst, fau)
+    compare_state(st, ost, 1e-5, fst)
     gs.step(st, au)
     osol.step(ost, oau)
-    compare_state(st, ost, 1e-4)
+    fsol.step(fst, fau)
+    compare_state(st, ost, 1e-4, fst)
     res = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=6, tol_rf=1e-300), dtype="f32").run()
     _, om, orec = O.NonblindSolver(oplan, f, probe, O.NonblindConfig(max_iters=6, tol_rf=1e-300)).run()
     assert rel_l2(res.merged, om) < 1e-3

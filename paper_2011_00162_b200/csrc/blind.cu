@@ -278,7 +278,12 @@ class Blind final : public BlindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
     R.reduce_rf(true);
     PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
-    // w-step
+    // w-step (blind.cpp:194-208): one launch where the frame fits a single-CTA engine
+    const cudaError_t we = launch_wstep<T>(R.S, wd_all_.as<cx<T>>(), R.D, mask_.as<T>(), R.tw.template as<cx<T>>(),
+                                           static_cast<T>(1.0 / static_cast<double>(R.S)), w_.as<cx<T>>(), R.skipB(), s);
+    if (we != cudaErrorNotSupported) {
+      PDD_CUDA(we);
+    } else {
     PDD_CUDA(launch_probe_avg<T>(wd_all_.as<cx<T>>(), R.D, static_cast<int>(SS), avg_.as<cx<T>>(), R.skipB(), s));
     FrameArgs<T> p1 = R.frame_args();
     p1.nframes = 1;
@@ -296,6 +301,7 @@ class Blind final : public BlindGpu {
     p2.frames_in = spec_.as<cx<T>>();
     p2.bp_out = w_.as<cx<T>>();
     PDD_CUDA(launch_frame<T>(kAdj, R.S, p2, s));
+    }
     // v-step from u^n, Lambda^n (blind.cpp:209-218).  Sequential here: the
     // blind image-side state is single-buffered (only Gamma ping-pongs), so
     // the v-step must see this iteration's stop decision (skipB).

@@ -276,6 +276,98 @@ cudaError_t launch_frame<double>(int mode, int S, const FrameArgs<double>& a, cu
 }
 
 // ---------------------------------------------------------------------------
+// Blind w-step in one launch (blind.cpp:194-208): avg = sum_d (Delta_d + W_d) / D
+// (d order) -> FFT2 -> support mask -> IFFT2 -> w.  One CTA, the frame engine
+// of fft.cuh; replaces probe_avg + forward + apply_mask + adjoint launches.
+template <typename T, int S, int R>
+__global__ void __launch_bounds__(Fft2<T, S, R>::NT) wstep_kernel(const cx<T>* wd_all, int D, const T* mask,
+                                                                  const cx<T>* twg, T scale, cx<T>* w,
+                                                                  const int* skip) {
+  using E = Fft2<T, S, R>;
+  constexpr int G = E::G, NT = E::NT;
+  extern __shared__ __align__(16) unsigned char wstep_smem[];
+  cx<T>* tws = reinterpret_cast<cx<T>*>(wstep_smem);
+  cx<T>* buf = tws + S;
+  if (skip && *skip) return;
+  const int t = threadIdx.x;
+  for (int i = t; i < S; i += NT) tws[i] = twg[i];
+  cx<T> v[R];
+  {
+    const int y = t / G, g = t % G;
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cx<T>{T(0), T(0)};
+    const cx<T>* src = wd_all + y * S + g;
+#pragma unroll 4
+    for (int d = 0; d < D; ++d) {  // d order per pixel; the R loads of a tile are independent
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] += src[static_cast<int64_t>(d) * S * S + G * m];
+    }
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cx<T>{v[m].x / static_cast<T>(D), v[m].y / static_cast<T>(D)};
+  }
+  __syncthreads();
+  E::forward(v, buf, tws, t);
+  {
+    const int x = t % S, c = t / S;
+#pragma unroll
+    for (int q = 0; q < R / G; ++q)
+#pragma unroll
+      for (int k1 = 0; k1 < G; ++k1) {
+        const int ky = (c + G * q) + R * k1;
+        const cx<T> val = v[q * G + k1] * scale;
+        v[q * G + k1] = mask[ky * S + x] == T(0) ? cx<T>{T(0), T(0)} : val;
+      }
+  }
+  __syncthreads();
+  E::inverse(v, buf, tws, t);
+  {
+    const int y = t / G, g = t % G;
+#pragma unroll
+    for (int m = 0; m < R; ++m) w[y * S + g + G * m] = v[m] * scale;
+  }
+}
+
+template <typename T, int S>
+static cudaError_t launch_wstep_s(const cx<T>* wd_all, int D, const T* mask, const cx<T>* tw, T scale, cx<T>* w,
+                                  const int* skip, cudaStream_t st) {
+  using C = FrameCfg<T, S>;
+  using E = Fft2<T, S, C::R>;
+  const size_t smem = sizeof(cx<T>) * (S + static_cast<size_t>(E::TILE));
+  auto kern = wstep_kernel<T, S, C::R>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  kern<<<1, E::NT, smem, st>>>(wd_all, D, mask, tw, scale, w, skip);
+  return cudaGetLastError();
+}
+
+// cudaErrorNotSupported: no single-CTA engine for this shape (complex128 128^2,
+// G == 1 shapes) -- the caller runs the four-launch w-step instead.
+template <>
+cudaError_t launch_wstep<float>(int S, const cx<float>* wd_all, int D, const float* mask, const cx<float>* tw,
+                                float scale, cx<float>* w, const int* skip, cudaStream_t st) {
+  switch (S) {
+    case 16: return launch_wstep_s<float, 16>(wd_all, D, mask, tw, scale, w, skip, st);
+    case 32: return launch_wstep_s<float, 32>(wd_all, D, mask, tw, scale, w, skip, st);
+    case 64: return launch_wstep_s<float, 64>(wd_all, D, mask, tw, scale, w, skip, st);
+  }
+  return cudaErrorNotSupported;
+}
+template <>
+cudaError_t launch_wstep<double>(int S, const cx<double>* wd_all, int D, const double* mask, const cx<double>* tw,
+                                 double scale, cx<double>* w, const int* skip, cudaStream_t st) {
+  switch (S) {
+    case 16: return launch_wstep_s<double, 16>(wd_all, D, mask, tw, scale, w, skip, st);
+    case 32: return launch_wstep_s<double, 32>(wd_all, D, mask, tw, scale, w, skip, st);
+    case 64: return launch_wstep_s<double, 64>(wd_all, D, mask, tw, scale, w, skip, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+// ---------------------------------------------------------------------------
 // block reduction of two doubles, fixed tree; result in thread 0.
 __device__ __forceinline__ void block_sum2(double& a, double& b, double* sm) {
 #pragma unroll

@@ -91,6 +91,11 @@ struct PairGeom {
 
 template <typename T>
 cudaError_t launch_frame(int mode, int S, const FrameArgs<T>& a, cudaStream_t st);
+// blind w-step (average of the D probe tiles -> FFT2 -> mask -> IFFT2 -> w) in one launch;
+// cudaErrorNotSupported for shapes without a single-CTA engine
+template <typename T>
+cudaError_t launch_wstep(int S, const cx<T>* wd_all, int D, const T* mask, const cx<T>* tw, T scale, cx<T>* w,
+                         const int* skip, cudaStream_t st);
 template <typename T>
 int sweep_stream_ctas(int S);  // persistent grid of the streamed SWEEP kernel (0: not streamed)
 template <typename T>

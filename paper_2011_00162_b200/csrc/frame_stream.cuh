@@ -377,6 +377,15 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int rb = 0; rb < NRB; ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
       cx<T> v[RR], pv[RR];
+      cx<T> pw2[RF2 ? RR : 1];
+      if constexpr (!TMEMP) {  // probe values from L2: in flight while the patch rows arrive
+        probe_row(f, rb, y, g, pv);
+        if constexpr (RF2) {
+          const cx<T>* pw = a.probe2 + y * S + g;
+#pragma unroll
+          for (int m = 0; m < RR; ++m) pw2[m] = pw[GR * m];
+        }
+      }
       if (tma_rows) {
         mbar_wait(s_rowbar + rb * NW + warp, row_phase);
 #pragma unroll
@@ -416,12 +425,11 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
       };
       if constexpr (RF2) {  // patch x shared probe -> rows of the second tile
         cx<T> v2[RR];
-        const cx<T>* pw = a.probe2 + y * S + g;
 #pragma unroll
-        for (int m = 0; m < RR; ++m) v2[m] = v[m] * pw[GR * m];
+        for (int m = 0; m < RR; ++m) v2[m] = v[m] * pw2[m];
         row_fft(v2, buf2);
       }
-      probe_row(f, rb, y, g, pv);
+      if constexpr (TMEMP) probe_row(f, rb, y, g, pv);
 #pragma unroll
       for (int m = 0; m < RR; ++m) v[m] = v[m] * pv[m];
       row_fft(v, buf);
@@ -662,7 +670,7 @@ __global__ void __launch_bounds__(SH::NT, SH::MINB) sweep_stream_kernel(const Fr
     for (int rb = 0; rb < (FWD ? 0 : NRB); ++rb) {
       const int y = rb * RPB + t / GR, g = t % GR;
       cx<T> v[RR], pv[RR];
-      probe_row(f, rb, y, g, pv);
+      if (TMEMP || !a.bp_raw) probe_row(f, rb, y, g, pv);  // blind: q_j is written without conj(probe)
 #pragma unroll
       for (int q = 0; q < RR / GR; ++q) {
         const int k2 = g + GR * q;

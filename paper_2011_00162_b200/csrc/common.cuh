@@ -576,7 +576,9 @@ struct RankData {
     g.sub_w = sub_w.as<int32_t>();
     g.sub_pbeg = sub_pbeg.as<int32_t>();
     g.ps = psides.as<PairSide>();
-    g.mbeg = fmeta_beg.as<int32_t>();  // covering frames (set_pieces switches to the pieces)
+    // covering frames, flattened (set_pieces switches to the pieces); chained
+    // layouts keep no flattened frame lists: the kernel then walks tile_frames
+    g.mbeg = L.fmeta_beg.empty() ? nullptr : fmeta_beg.as<int32_t>();
     g.meta = fmeta.as<int4>();
     g.mbase = fmeta_base.as<int64_t>();
     g.tps_beg = tps_beg.as<int32_t>();

@@ -58,21 +58,32 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int
   for (int ld = 0; ld < L.nls(); ++ld) {
     const int64_t H = L.sub_h[ld], W = L.sub_w[ld];
     const int64_t ntr = (H + th - 1) / th, ntc = (W + tw - 1) / tw;
-    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(ntr * ntc));
-    for (int64_t f = L.sub_fr_beg[ld]; f < L.sub_fr_beg[ld + 1]; ++f) {
+    // covering frames per tile, ascending f: counting pass, prefix sums, fill
+    // (one flat array; a vector per tile cost ~10 ms of host time on config 4)
+    std::vector<int32_t> cnt(static_cast<size_t>(ntr * ntc) + 1, 0);
+    auto tiles_of = [&](int64_t f, auto&& fn) {
       const int64_t r0 = L.fr_r[f], c0 = L.fr_c[f];
       const int64_t tr_a = r0 / th, tr_b = std::min(ntr - 1, (r0 + L.S - 1) / th);
       const int64_t tc_a = c0 / tw, tc_b = std::min(ntc - 1, (c0 + L.S - 1) / tw);
       for (int64_t tr = tr_a; tr <= tr_b; ++tr)
-        for (int64_t tc = tc_a; tc <= tc_b; ++tc) lists[tr * ntc + tc].push_back(static_cast<int32_t>(f));
-    }
+        for (int64_t tc = tc_a; tc <= tc_b; ++tc) fn(tr * ntc + tc);
+    };
+    for (int64_t f = L.sub_fr_beg[ld]; f < L.sub_fr_beg[ld + 1]; ++f)
+      tiles_of(f, [&](int64_t tile) { ++cnt[static_cast<size_t>(tile) + 1]; });
+    for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+    const size_t base0 = L.tile_frames.size();
+    L.tile_frames.resize(base0 + static_cast<size_t>(cnt.back()));
     for (int64_t tr = 0; tr < ntr; ++tr)
-      for (int64_t tc = 0; tc < ntc; ++tc) {
-        const auto& l = lists[tr * ntc + tc];
+      for (int64_t tc = 0; tc < ntc; ++tc)
         L.tiles.push_back(int4{ld, static_cast<int>(tr * th), static_cast<int>(tc * tw),
-                               static_cast<int>(L.tile_frames.size())});
-        L.tile_frames.insert(L.tile_frames.end(), l.begin(), l.end());
-      }
+                               static_cast<int>(base0 + static_cast<size_t>(cnt[static_cast<size_t>(tr * ntc + tc)]))});
+    {
+      std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+      for (int64_t f = L.sub_fr_beg[ld]; f < L.sub_fr_beg[ld + 1]; ++f)
+        tiles_of(f, [&](int64_t tile) {
+          L.tile_frames[base0 + static_cast<size_t>(cur[static_cast<size_t>(tile)]++)] = static_cast<int32_t>(f);
+        });
+    }
     L.sub_tile_beg.push_back(static_cast<int64_t>(L.tiles.size()));
   }
   L.tiles.push_back(int4{0, 0, 0, static_cast<int>(L.tile_frames.size())});
@@ -152,7 +163,6 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int
     for (int ld = 0; ld < L.nls(); ++ld) {
       const int64_t H = L.sub_h[ld], W = L.sub_w[ld];
       const int64_t ntr = (H + th - 1) / th, ntc = (W + tw - 1) / tw;
-      std::vector<std::vector<int32_t>> lists(static_cast<size_t>(ntr * ntc));
       int k1 = k0;
       while (k1 < L.npieces() && L.fr_sub[L.pc_pos[L.pc_beg[k1]].x] == ld) ++k1;
       std::vector<int32_t> ids;
@@ -160,17 +170,25 @@ Layout Layout::build(const Plan& plan, int rank, int world, bool allow_wide, int
       std::stable_sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
         return L.it_c[a] != L.it_c[b] ? L.it_c[a] < L.it_c[b] : L.it_r[a] < L.it_r[b];
       });
-      for (int32_t k : ids) {
+      // counting pass, prefix sums, fill (ids order within each tile)
+      auto tiles_of = [&](int32_t k, auto&& fn) {
         const int64_t r0 = L.it_r[k], c0 = L.it_c[k];
         const int64_t tr_a = r0 / th, tr_b = std::min(ntr - 1, (r0 + L.it_h[k] - 1) / th);
         const int64_t tc_a = c0 / tw, tc_b = std::min(ntc - 1, (c0 + S - 1) / tw);
         for (int64_t tr = tr_a; tr <= tr_b; ++tr)
-          for (int64_t tc = tc_a; tc <= tc_b; ++tc) lists[tr * ntc + tc].push_back(k);
+          for (int64_t tc = tc_a; tc <= tc_b; ++tc) fn(tr * ntc + tc);
+      };
+      std::vector<int32_t> cnt(static_cast<size_t>(ntr * ntc) + 1, 0);
+      for (int32_t k : ids) tiles_of(k, [&](int64_t tile) { ++cnt[static_cast<size_t>(tile) + 1]; });
+      for (size_t q = 1; q < cnt.size(); ++q) cnt[q] += cnt[q - 1];
+      const size_t base0 = L.tile_items.size();
+      L.tile_items.resize(base0 + static_cast<size_t>(cnt.back()));
+      {
+        std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+        for (int32_t k : ids)
+          tiles_of(k, [&](int64_t tile) { L.tile_items[base0 + static_cast<size_t>(cur[static_cast<size_t>(tile)]++)] = k; });
       }
-      for (const auto& l : lists) {
-        L.tile_items.insert(L.tile_items.end(), l.begin(), l.end());
-        L.tile_item_beg.push_back(static_cast<int32_t>(L.tile_items.size()));
-      }
+      for (size_t q = 1; q < cnt.size(); ++q) L.tile_item_beg.push_back(static_cast<int32_t>(base0) + cnt[q]);
       k0 = k1;
     }
   }
@@ -245,13 +263,30 @@ void Layout::flatten_gather_lists() {
   fmeta_base.clear();
   imeta_base.clear();
   tps.clear();
+  // chained layouts: the update pass walks the pieces (imeta); the per-frame
+  // lists are then only read by the one-off density gather at setup, which
+  // takes them from tile_frames directly (no flattened copy: 15 MB on config 4)
+  const bool frames_flat = !chained;
+  if (frames_flat) {
+    fmeta.reserve(tile_frames.size());
+    fmeta_base.reserve(tile_frames.size());
+    fmeta_beg.reserve(static_cast<size_t>(ntiles()) + 1);
+  } else {
+    fmeta_beg.clear();
+    imeta.reserve(tile_items.size());
+    imeta_base.reserve(tile_items.size());
+    imeta_beg.reserve(static_cast<size_t>(ntiles()) + 1);
+  }
+  tps_beg.reserve(static_cast<size_t>(ntiles()) + 1);
   for (int t = 0; t < ntiles(); ++t) {
-    for (int k = tiles[t].w; k < tiles[t + 1].w; ++k) {
-      const int f = tile_frames[k];
-      fmeta.push_back(int4{fr_r[f], fr_c[f], S, f});
-      fmeta_base.push_back(static_cast<int64_t>(f) * SS);
+    if (frames_flat) {
+      for (int k = tiles[t].w; k < tiles[t + 1].w; ++k) {
+        const int f = tile_frames[k];
+        fmeta.push_back(int4{fr_r[f], fr_c[f], S, f});
+        fmeta_base.push_back(static_cast<int64_t>(f) * SS);
+      }
+      fmeta_beg.push_back(static_cast<int32_t>(fmeta.size()));
     }
-    fmeta_beg.push_back(static_cast<int32_t>(fmeta.size()));
     if (chained) {
       for (int k = tile_item_beg[t]; k < tile_item_beg[t + 1]; ++k) {
         const int it = tile_items[k];

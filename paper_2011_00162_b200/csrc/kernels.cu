@@ -417,8 +417,18 @@ __device__ __forceinline__ cx<T>& operator+=(cx<T>& a, typename Vec2<T>::type b)
 // MODE is a template parameter: the accumulation loop then holds no branches,
 // so the NROW x unroll predicated loads of one trip are all in flight before
 // the first add waits on one of them.
+//
+// Resident CTAs asked of ptxas: 4 (64 registers) for the overlap-add modes and
+// for the small-tile float blind update (config 3: 59 -> 54 us; the larger
+// tiles and complex128 would spill at 64 registers).
 template <typename T, int NROW, int VEC, int MODE>
-__global__ void __launch_bounds__(256, (MODE == kGatherNonblind || MODE == kGatherAdjoint) ? 4 : 1) gather_kernel(const GatherArgs<T> a) {
+constexpr int gather_min_ctas() {
+  if (MODE == kGatherNonblind || MODE == kGatherAdjoint) return 4;
+  if (MODE == kGatherBlind && sizeof(T) == 4 && NROW * VEC <= 2) return 4;
+  return 1;
+}
+template <typename T, int NROW, int VEC, int MODE>
+__global__ void __launch_bounds__(256, gather_min_ctas<T, NROW, VEC, MODE>()) gather_kernel(const GatherArgs<T> a) {
   constexpr int kMeta = 256;  // covering frames staged in shared memory per chunk
   __shared__ double sm[16];
   __shared__ int s_fr[kMeta], s_r0[kMeta], s_c0[kMeta], s_h[kMeta];

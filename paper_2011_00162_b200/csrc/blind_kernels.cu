@@ -26,6 +26,7 @@ __global__ void probe_partials_kernel(const cx<T>* img, const int64_t* off, cons
   const int f0 = chunk_f0[c], f1 = chunk_f1[c];
   cx<T> num{T(0), T(0)};
   T den = T(0);
+#pragma unroll 8  // eight frames' loads in flight; the adds keep their order
   for (int f = f0; f < f1; ++f) {
     const cx<T> qq = q[static_cast<int64_t>(f) * SS + pix];
     if (mode == 1) {

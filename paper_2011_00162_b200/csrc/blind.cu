@@ -276,8 +276,7 @@ class Blind final : public BlindGpu {
     R.set_pieces(a);  // streamed sweep schedule (one piece per frame: q_j stays per frame)
     PDD_CUDA(launch_frame<T>(kBlind, R.S, a, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
-    R.reduce_rf(true);
-    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_rf_finalize();
     // w-step (blind.cpp:194-208): one launch where the frame fits a single-CTA engine
     const cudaError_t we = launch_wstep<T>(R.S, wd_all_.as<cx<T>>(), R.D, mask_.as<T>(), R.tw.template as<cx<T>>(),
                                            static_cast<T>(1.0 / static_cast<double>(R.S)), w_.as<cx<T>>(), R.skipB(), s);
@@ -334,8 +333,7 @@ class Blind final : public BlindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[2], s));
     PDD_CUDA(launch_gather<T>(g, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[3], s));
-    R.reduce_re();
-    PDD_CUDA(launch_re_finalize(R.ctlp(), R.diff_sub(), R.norm_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_re_finalize();
   }
 
   void enqueue_tail() {  // R-factor of the current iterate with the shared probe
@@ -347,8 +345,7 @@ class Blind final : public BlindGpu {
     a.rf_part = R.rf_part.template as<double>();
     a.stop_flag = R.skipA();
     PDD_CUDA(launch_frame<T>(kFwd, R.S, a, s));
-    R.reduce_rf(true);
-    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_rf_finalize();
   }
 
   void ensure_graphs() {
@@ -583,8 +580,13 @@ class Blind final : public BlindGpu {
   void sync() override { R.stream.sync(); }
   // float32 s = 64: the BLIND frame pass is two streamed launches (kernels.cu)
   void* stream() const override { return R.st(); }
+  // gate; frame pass (two launches only for complex128 128^2); R-factor sums + finalize (1 fused / 2);
+  // w-step (1 where wstep_kernel applies, else 4); pack, vstep; probe partials, chunk reduce, probe
+  // update; update pass; RE sums + finalize (1 fused / 3)
   int64_t kernel_launches_per_iteration() const override {
-    return std::is_same_v<T, float> && R.S == 64 ? 18 : 17;
+    const int frame = (std::is_same_v<T, double> && R.S == 128) ? 2 : 1;
+    const int wstep = (R.S == 16 || R.S == 32 || R.S == 64) ? 1 : 4;
+    return 1 + frame + (R.fused_finalize() ? 1 : 2) + wstep + 2 + 3 + 1 + (R.fused_finalize() ? 1 : 3);
   }
 
  private:

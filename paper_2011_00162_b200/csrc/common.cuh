@@ -312,6 +312,7 @@ struct RankData {
   DevMem pc_beg, pc_pos, pc_ofs, pc_rec, it_r, it_c, it_h, it_base, tile_items, tile_item_beg;  // back-projection pieces
   DevMem fmeta_beg, fmeta, fmeta_base, imeta_beg, imeta, imeta_base, tps_beg, tps;  // flattened gather lists
   DevMem rf_part, re_part, sums;  // sums: [3][D] = rf, diff, norm per subdomain
+  DevMem fin_counter;
   DevMem scratch;  // global transpose tiles of the streamed kernel (complex128 128^2 frames)
   DevMem ctl, rec;
   DevMem pin_dev;  // uint8 per local image pixel
@@ -403,6 +404,8 @@ struct RankData {
     PDD_CUDA(cudaMemsetAsync(sums.get(), 0, sums.bytes(), s));
     ctl.alloc(sizeof(RunCtl));
     PDD_CUDA(cudaMemsetAsync(ctl.get(), 0, sizeof(RunCtl), s));
+    fin_counter.alloc(sizeof(unsigned));  // segsum_finalize_kernel's last-block counter (self-resetting)
+    PDD_CUDA(cudaMemsetAsync(fin_counter.get(), 0, sizeof(unsigned), s));
     rec_cap = max_iters + 2;
     rec.alloc(sizeof(double) * 2 * static_cast<size_t>(rec_cap));
 
@@ -593,6 +596,32 @@ struct RankData {
     PDD_CUDA(launch_segsum(rf_part.as<double>(), 1, 0, sub_fr_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
                            rf_sub(), gated ? skipA() : nullptr, s));
     if (comm) comm->allreduce_sum_f64(rf_sub(), D, s);
+  }
+  // reduce + finalize of the iteration's R-factor / RE.  Single-rank solvers
+  // run them as one launch each (segsum_finalize_kernel); with a communicator
+  // the all-reduce sits between the sums and the finalize step.
+  bool fused_finalize() const { return !comm && D <= fused_finalize_max_subdomains(); }
+  void reduce_rf_finalize() {
+    cudaStream_t s = st();
+    if (!fused_finalize()) {
+      reduce_rf(true);
+      PDD_CUDA(launch_rf_finalize(ctlp(), rf_sub(), D, rec.template as<double>(), s));
+      return;
+    }
+    PDD_CUDA(launch_segsum_finalize(1, rf_part.as<double>(), sub_fr_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                                    rf_sub(), nullptr, skipA(), fin_counter.as<unsigned>(), ctlp(), D,
+                                    rec.template as<double>(), s));
+  }
+  void reduce_re_finalize() {
+    cudaStream_t s = st();
+    if (!fused_finalize()) {
+      reduce_re();
+      PDD_CUDA(launch_re_finalize(ctlp(), diff_sub(), norm_sub(), D, rec.template as<double>(), s));
+      return;
+    }
+    PDD_CUDA(launch_segsum_finalize(2, re_part.as<double>(), sub_tile_beg.as<int64_t>(), L.nls(), local_map.as<int>(),
+                                    diff_sub(), norm_sub(), skipB(), fin_counter.as<unsigned>(), ctlp(), D,
+                                    rec.template as<double>(), s));
   }
   void reduce_re() {
     cudaStream_t s = st();

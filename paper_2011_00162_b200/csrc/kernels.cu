@@ -1018,7 +1018,7 @@ __global__ void gate_kernel(RunCtl* c) {
   c->skipB = c->stop != 0;
   c->skipC = c->stop != 0;
 }
-__global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, double* rec) {
+__device__ __forceinline__ void rf_finalize_body(RunCtl* c, const double* rf_sub, int D, double* rec) {
   if (c->skipA) return;
   double s = 0.0;
   for (int d = 0; d < D; ++d) s += rf_sub[d];
@@ -1039,7 +1039,10 @@ __global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, doubl
   }
   c->skipB = c->stop != 0;
 }
-__global__ void re_finalize_kernel(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
+__global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, double* rec) {
+  rf_finalize_body(c, rf_sub, D, rec);
+}
+__device__ __forceinline__ void re_finalize_body(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
   if (c->skipB) return;
   double re = 0.0;
   bool finite = true;
@@ -1060,6 +1063,63 @@ __global__ void re_finalize_kernel(RunCtl* c, const double* diff, const double* 
     c->stop = n;
   }
 }
+__global__ void re_finalize_kernel(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
+  re_finalize_body(c, diff, norm, D, rec);
+}
+
+// Segment sums and the finalize step in ONE launch (single-rank solvers: no
+// all-reduce sits between them): block b sums segment b exactly as
+// segsum_kernel does (same strided accumulation and tree, so the sums are
+// bit-identical to the two-launch path of multi-rank solvers), and the block
+// that finishes last -- a device counter it resets -- runs the finalize body
+// on the D sums.  NCOMP = 1: R-factor numerators; NCOMP = 2: RE (diff, norm).
+constexpr int kFusedMaxD = 64;
+template <int NCOMP>
+__global__ void segsum_finalize_kernel(const double* in, const int64_t* beg, const int* map, double* out0, double* out1,
+                                       const int* skip, unsigned* counter, RunCtl* c, int D, double* rec) {
+  __shared__ double sm[16];
+  __shared__ double fin[2 * kFusedMaxD];
+  __shared__ int last;
+  if (skip && *skip) return;
+  const int64_t b = beg[blockIdx.x], e = beg[blockIdx.x + 1];
+  double acc0 = 0.0, acc1 = 0.0;
+  // (the two components of block_sum2 are summed independently, each with
+  // the per-thread order and tree segsum_kernel gives it)
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+    acc0 += in[NCOMP * i];
+    if constexpr (NCOMP == 2) acc1 += in[2 * i + 1];
+  }
+  block_sum2(acc0, acc1, sm);
+  if (threadIdx.x == 0) {
+    const int o = map ? map[blockIdx.x] : blockIdx.x;
+    out0[o] = acc0;
+    if constexpr (NCOMP == 2) out1[o] = acc1;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < D) {
+    fin[threadIdx.x] = __ldcg(out0 + threadIdx.x);
+    if constexpr (NCOMP == 2) fin[kFusedMaxD + threadIdx.x] = __ldcg(out1 + threadIdx.x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if constexpr (NCOMP == 1) rf_finalize_body(c, fin, D, rec);
+    else re_finalize_body(c, fin, fin + kFusedMaxD, D, rec);
+  }
+}
+cudaError_t launch_segsum_finalize(int ncomp, const double* in, const int64_t* beg, int nseg, const int* map,
+                                   double* out0, double* out1, const int* skip, unsigned* counter, RunCtl* c, int D,
+                                   double* rec, cudaStream_t st) {
+  if (nseg <= 0 || D > kFusedMaxD || D > 256) return cudaErrorInvalidValue;
+  if (ncomp == 1) segsum_finalize_kernel<1><<<nseg, 256, 0, st>>>(in, beg, map, out0, out1, skip, counter, c, D, rec);
+  else segsum_finalize_kernel<2><<<nseg, 256, 0, st>>>(in, beg, map, out0, out1, skip, counter, c, D, rec);
+  return cudaGetLastError();
+}
+int fused_finalize_max_subdomains() { return kFusedMaxD; }
 cudaError_t launch_gate(RunCtl* c, cudaStream_t st) {
   gate_kernel<<<1, 1, 0, st>>>(c);
   return cudaGetLastError();

@@ -186,5 +186,11 @@ cudaError_t launch_gate(RunCtl* c, cudaStream_t st);
 cudaError_t launch_rf_finalize(RunCtl* c, const double* rf_sub, int D, double* rec, cudaStream_t st);
 cudaError_t launch_re_finalize(RunCtl* c, const double* diff, const double* norm, int D, double* rec,
                                cudaStream_t st);
+// segsum + finalize in one launch (single-rank solvers, D <= fused_finalize_max_subdomains()):
+// ncomp 1 = R-factor (out0), 2 = RE (out0 = diff, out1 = norm); counter: a zeroed device word
+cudaError_t launch_segsum_finalize(int ncomp, const double* in, const int64_t* beg, int nseg, const int* map,
+                                   double* out0, double* out1, const int* skip, unsigned* counter, RunCtl* c, int D,
+                                   double* rec, cudaStream_t st);
+int fused_finalize_max_subdomains();
 
 }  // namespace pdd

@@ -191,8 +191,7 @@ class Nonblind final : public NonblindGpu {
     R.set_pieces(a);
     PDD_CUDA(launch_frame<T>(kSweep, R.S, a, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[1], s));
-    R.reduce_rf(true);
-    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_rf_finalize();
     R.join_consensus();
     GatherArgs<T> g = R.gather_args(kGatherNonblind);
     R.set_pieces(g);
@@ -210,8 +209,7 @@ class Nonblind final : public NonblindGpu {
     if (ev) PDD_CUDA(cudaEventRecord(ev[2], s));
     PDD_CUDA(launch_gather<T>(g, s));
     if (ev) PDD_CUDA(cudaEventRecord(ev[3], s));
-    R.reduce_re();
-    PDD_CUDA(launch_re_finalize(R.ctlp(), R.diff_sub(), R.norm_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_re_finalize();
   }
 
   // Frame pass only: records the R-factor of the current iterate.
@@ -224,8 +222,7 @@ class Nonblind final : public NonblindGpu {
     a.rf_part = R.rf_part.template as<double>();
     a.stop_flag = R.skipA();
     PDD_CUDA(launch_frame<T>(kFwd, R.S, a, s));
-    R.reduce_rf(true);
-    PDD_CUDA(launch_rf_finalize(R.ctlp(), R.rf_sub(), R.D, R.rec.template as<double>(), s));
+    R.reduce_rf_finalize();
   }
 
   void ensure_graphs() {
@@ -557,7 +554,9 @@ class Nonblind final : public NonblindGpu {
   }
   void sync() override { R.stream.sync(); }
   void* stream() const override { return R.st(); }
-  int64_t kernel_launches_per_iteration() const override { return 10; }
+  // gate, pack, vstep, sweep, R-factor sums + finalize (one launch when fused, else two), update pass,
+  // RE sums + finalize (one launch when fused, else three)
+  int64_t kernel_launches_per_iteration() const override { return R.fused_finalize() ? 7 : 10; }
 
  private:
   Plan plan_;

@@ -257,7 +257,7 @@ class Blind final : public BlindGpu {
   void enqueue_iteration(int parity, bool store_z, cudaEvent_t* ev = nullptr) {
     cudaStream_t s = R.st();
     const int64_t SS = R.SS();
-    PDD_CUDA(launch_gate(R.ctlp(), s));
+    // (the pass switches were set by reset_ctl or by the previous iteration's RE finalize step)
     if (ev) PDD_CUDA(cudaEventRecord(ev[0], s));
     FrameArgs<T> a = R.frame_args();
     a.probe = wc_.as<cx<T>>();
@@ -580,13 +580,13 @@ class Blind final : public BlindGpu {
   void sync() override { R.stream.sync(); }
   // float32 s = 64: the BLIND frame pass is two streamed launches (kernels.cu)
   void* stream() const override { return R.st(); }
-  // gate; frame pass (two launches only for complex128 128^2); R-factor sums + finalize (1 fused / 2);
+  // frame pass (two launches only for complex128 128^2); R-factor sums + finalize (1 fused / 2);
   // w-step (1 where wstep_kernel applies, else 4); pack, vstep; probe partials, chunk reduce, probe
   // update; update pass; RE sums + finalize (1 fused / 3)
   int64_t kernel_launches_per_iteration() const override {
     const int frame = (std::is_same_v<T, double> && R.S == 128) ? 2 : 1;
     const int wstep = (R.S == 16 || R.S == 32 || R.S == 64) ? 1 : 4;
-    return 1 + frame + (R.fused_finalize() ? 1 : 2) + wstep + 2 + 3 + 1 + (R.fused_finalize() ? 1 : 3);
+    return frame + (R.fused_finalize() ? 1 : 2) + wstep + 2 + 3 + 1 + (R.fused_finalize() ? 1 : 3);
   }
 
  private:

@@ -1013,11 +1013,15 @@ cudaError_t launch_rpen_sub(const uint8_t* pin, const PairSide* ps, int nps, int
 
 // ---------------------------------------------------------------------------
 // iteration control: stop rules of run() (solver.cpp:225-262) on the device
-__global__ void gate_kernel(RunCtl* c) {
+// Switches of the NEXT iteration's passes from the run state.  Runs at the end
+// of every RE finalize step (so an iteration needs no launch of its own for
+// it) and as gate_kernel before the trailing R-factor pass.
+__device__ __forceinline__ void gate_body(RunCtl* c) {
   c->skipA = !(c->stop == 0 || (c->stop == c->iter && !c->done));
   c->skipB = c->stop != 0;
   c->skipC = c->stop != 0;
 }
+__global__ void gate_kernel(RunCtl* c) { gate_body(c); }
 __device__ __forceinline__ void rf_finalize_body(RunCtl* c, const double* rf_sub, int D, double* rec) {
   if (c->skipA) return;
   double s = 0.0;
@@ -1043,7 +1047,10 @@ __global__ void rf_finalize_kernel(RunCtl* c, const double* rf_sub, int D, doubl
   rf_finalize_body(c, rf_sub, D, rec);
 }
 __device__ __forceinline__ void re_finalize_body(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
-  if (c->skipB) return;
+  if (c->skipB) {
+    gate_body(c);
+    return;
+  }
   double re = 0.0;
   bool finite = true;
   for (int d = 0; d < D; ++d) {
@@ -1062,6 +1069,7 @@ __device__ __forceinline__ void re_finalize_body(RunCtl* c, const double* diff, 
   } else if (n >= c->max_iters) {
     c->stop = n;
   }
+  gate_body(c);
 }
 __global__ void re_finalize_kernel(RunCtl* c, const double* diff, const double* norm, int D, double* rec) {
   re_finalize_body(c, diff, norm, D, rec);
@@ -1080,7 +1088,10 @@ __global__ void segsum_finalize_kernel(const double* in, const int64_t* beg, con
   __shared__ double sm[16];
   __shared__ double fin[2 * kFusedMaxD];
   __shared__ int last;
-  if (skip && *skip) return;
+  if (skip && *skip) {  // pass disabled: only the RE step's closing gate remains to do
+    if (NCOMP == 2 && blockIdx.x == 0 && threadIdx.x == 0) gate_body(c);
+    return;
+  }
   const int64_t b = beg[blockIdx.x], e = beg[blockIdx.x + 1];
   double acc0 = 0.0, acc1 = 0.0;
   // (the two components of block_sum2 are summed independently, each with

@@ -171,7 +171,7 @@ class Nonblind final : public NonblindGpu {
   // profiling only): events recorded around the frame and gather kernels.
   void enqueue_iteration(int parity, bool store_z, cudaEvent_t* ev = nullptr) {
     cudaStream_t s = R.st();
-    PDD_CUDA(launch_gate(R.ctlp(), s));
+    // (the pass switches were set by reset_ctl or by the previous iteration's RE finalize step)
     // v^{n+1} from u^n, Lambda^n (solver.cpp:141-151) into the outgoing
     // parity, on a branch concurrent with the frame pass
     R.fork_consensus(U(parity), LAM(parity), s_.as<cx<T>>(), V(1 - parity));
@@ -554,9 +554,9 @@ class Nonblind final : public NonblindGpu {
   }
   void sync() override { R.stream.sync(); }
   void* stream() const override { return R.st(); }
-  // gate, pack, vstep, sweep, R-factor sums + finalize (one launch when fused, else two), update pass,
+  // pack, vstep, sweep, R-factor sums + finalize (one launch when fused, else two), update pass,
   // RE sums + finalize (one launch when fused, else three)
-  int64_t kernel_launches_per_iteration() const override { return R.fused_finalize() ? 7 : 10; }
+  int64_t kernel_launches_per_iteration() const override { return R.fused_finalize() ? 6 : 9; }
 
  private:
   Plan plan_;
